@@ -1,0 +1,433 @@
+#!/usr/bin/env python3
+"""Benchmark of the CountSketch S.A hot path (BASELINE.json metric:
+"CountSketch S.A nonzeros/sec and % of HBM roofline at 1/2/4/8 B200").
+
+Default workload = BASELINE config 3 (the config the metric's 1/2/4/8-GPU
+clause is quoted on): dense fp32 A, n = 16,777,216 x d = 128 (8.6 GB), rows
+N(0,1) scaled by lognormal(0,1), CountSketch m = 65,536; S.A only, rows
+sharded across the N ranks, partial m x d SA all-reduced with NCCL (strong
+scaling: total n fixed).  A step = one S.A over the rank's shard (+ the
+all-reduce when N > 1), inputs resident in HBM.  Each SA entry is accumulated
+in fp64 in ascending row order (bit-identical to the reference) and written
+as fp32.  Synthetic data (no dataset is named); inputs (8.6 GB) exceed the
+126 MB L2, so no flush is needed between steps.
+
+Run:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+      torchrun --nproc-per-node N bench.py --gpus N ...
+Other configs for profiling: --config c1|c2|c4 (not the headline line).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CountSketch S·A nonzeros/sec and % of HBM roofline at 1/2/4/8 B200"
+CONFIGS = {
+    "c1": dict(kind="dense", n=100_000, d=20, m=4_000, dtype="f64", seed=1,
+               workload="config1: dense fp64 100000x20 N(0,1), m=4000"),
+    "c2": dict(kind="csr", n=1_000_000, d=50, m=25_000, dtype="f64", per_row=5, seed=1,
+               workload="config2: CSR fp64 1000000x50, 5 nnz/row, m=25000"),
+    "c3": dict(kind="dense", n=16_777_216, d=128, m=65_536, dtype="f32", seed=1, lognormal=True,
+               workload="config3: dense fp32 16777216x128 (rows N(0,1)*lognormal(0,1)), m=65536, S.A row-sharded + all-reduce"),
+    "c4": dict(kind="csr", n=4_194_304, d=64, m=16_384, dtype="f32", per_row=16, dense_frac=0.01, seed=1,
+               workload="config4: CSR fp32 4194304x64, 16 nnz/row + 1% dense rows N(0,100), m=16384"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampler thread: SM clock + throttle reasons during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake_slowdown": 0x80}
+    OTHER = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+             "sync_boost": 0x10, "display_clock_setting": 0x100}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log("nvml unavailable:", e)
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in {**self.BAD, **self.OTHER}.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons - {"gpu_idle"}),
+                "samples": len(self.samples)}
+
+    def rejected(self):
+        if self.reasons & set(self.BAD):
+            return True
+        s = self.summary()
+        return bool(s["sm_mhz"] and s["sm_max_mhz"] and s["sm_mhz"] < 0.5 * s["sm_max_mhz"]
+                    and "sw_power_cap" not in self.reasons)
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_for(cfg_name: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- data
+def gen_dense_shard(torch, cfg, r0, r1, device):
+    """Rows [r0, r1) of the synthetic A; generated in fixed 2^20-row blocks with
+    per-block seeds, so any sharding yields the same global matrix."""
+    blk = 1 << 20
+    dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    out = torch.empty((r1 - r0, cfg["d"]), dtype=dt, device=device)
+    g = torch.Generator(device=device)
+    for b0 in range((r0 // blk) * blk, r1, blk):
+        b1 = min(b0 + blk, cfg["n"])
+        g.manual_seed(1_000_003 * (b0 // blk) + 17)
+        x = torch.randn((b1 - b0, cfg["d"]), generator=g, device=device, dtype=torch.float32)
+        if cfg.get("lognormal"):
+            x *= torch.exp(torch.randn((b1 - b0, 1), generator=g, device=device, dtype=torch.float32))
+        lo, hi = max(b0, r0), min(b1, r1)
+        out[lo - r0 : hi - r0] = x[lo - b0 : hi - b0].to(dt)
+    return out
+
+
+def gen_csr_shard(torch, cfg, r0, r1, device):
+    """CSR rows [r0, r1): `per_row` distinct uniform columns per row, N(0,1)
+    values; a `dense_frac` of rows fully dense with N(0, 100) values (c4)."""
+    d, per = cfg["d"], cfg["per_row"]
+    dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(7_000_003 + r0)
+    m = r1 - r0
+    dense_rows = torch.zeros(m, dtype=torch.bool, device=device)
+    if cfg.get("dense_frac"):
+        dense_rows = torch.rand(m, generator=g, device=device) < cfg["dense_frac"]
+    keys = torch.rand((m, d), generator=g, device=device)
+    sel = torch.zeros((m, d), dtype=torch.bool, device=device)
+    top = torch.topk(keys, per, dim=1).indices
+    sel.scatter_(1, top, True)
+    sel |= dense_rows[:, None]
+    counts = sel.sum(1)
+    indptr = torch.zeros(m + 1, dtype=torch.int64, device=device)
+    indptr[1:] = torch.cumsum(counts, 0)
+    indices = sel.nonzero()[:, 1].to(torch.int32)
+    nnz = int(indptr[-1])
+    row_of = torch.repeat_interleave(torch.arange(m, device=device), counts)
+    scale = torch.where(dense_rows[row_of], 10.0, 1.0)
+    vals = (torch.randn(nnz, generator=g, device=device) * scale).to(dt)
+    if nnz < 2**31:
+        indptr = indptr.to(torch.int32)
+    return indptr, indices, vals
+
+
+# ---------------------------------------------------------------- arms
+def reference_arm(args, cfg):
+    """The reference's CPU implementation of the path on this host: the oracle
+    port with the reference's own primitives (scipy CSR @ dense after the fp64
+    upcast + finiteness scan; repeat + bincount for CSR), single-threaded by
+    construction.  Each step = one bounded sample of the workload."""
+    import numpy as np
+    import scipy.sparse as sp
+
+    from oracle import oracle as O
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    sample_rows = {"c1": cfg["n"], "c2": cfg["n"], "c3": 1 << 18, "c4": 1 << 18}[args.config]
+    rng = np.random.default_rng(5)
+    h, s = O.hash_signs(sample_rows, cfg["m"], cfg["seed"])
+    mat = O.np_sketch_matrix(h, s, cfg["m"], sample_rows)
+    npdt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    if cfg["kind"] == "dense":
+        a = rng.standard_normal((sample_rows, cfg["d"])).astype(npdt)
+        if args.config == "c3":
+            a *= np.exp(rng.standard_normal((sample_rows, 1))).astype(npdt)
+        nnz = a.size
+        step = lambda: O.np_apply_dense(mat, a)  # noqa: E731
+    else:
+        from tests.synth import csr_fixed_nnz
+
+        a = csr_fixed_nnz(rng, sample_rows, cfg["d"], cfg["per_row"], dtype=npdt)
+        nnz = a.nnz
+        step = lambda: O.np_apply_csr(h, s, cfg["m"], a)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = nnz * args.steps / dt
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "sample_rows": sample_rows, "d": cfg["d"], "m": cfg["m"]},
+        "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": "port",
+                         "sample": f"first {sample_rows} rows of the workload (same m, d, distribution); "
+                                   "reference primitives, single-threaded"},
+        "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def cpu_baseline_sample(cfg_name, cfg, a_dev_sample, torch):
+    """Oracle port (reference primitives) timed on this host over a bounded
+    sample (~10-30 s of CPU work)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    a = a_dev_sample.cpu().numpy()
+    rows = a.shape[0]
+    h, s = O.hash_signs(rows, cfg["m"], cfg["seed"])
+    mat = O.np_sketch_matrix(h, s, cfg["m"], rows)
+    best = float("inf")
+    t_end = time.perf_counter() + 12.0
+    reps = 0
+    while reps < 2 or (time.perf_counter() < t_end and reps < 20):
+        t0 = time.perf_counter()
+        O.np_apply_dense(mat, a)
+        best = min(best, time.perf_counter() - t0)
+        reps += 1
+    return {"value": a.size / best, "unit": "nnz/s", "cores": 1, "kind": "port",
+            "sample": f"rows [0, {rows}) of the workload x {cfg['d']} cols, best of {reps} "
+                      "(scipy CSR @ dense after fp64 upcast, the reference's sketch.py:165 path)"}
+
+
+def our_arm(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1207_6365_b200 import SparseEmbedding, launch_count
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, d, m = cfg["n"], cfg["d"], cfg["m"]
+    r0, r1 = rank * n // world, (rank + 1) * n // world
+    sa_dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+
+    # ---- inputs resident in HBM
+    if cfg["kind"] == "dense":
+        A = gen_dense_shard(torch, cfg, r0, r1, dev)
+        nnz_local = A.numel()
+        in_bytes = A.numel() * A.element_size()
+    else:
+        ip, ix, vv = gen_csr_shard(torch, cfg, r0, r1, dev)
+        nnz_local = vv.numel()
+        in_bytes = vv.numel() * (vv.element_size() + 4) + ip.numel() * ip.element_size()
+    torch.cuda.synchronize()
+
+    # ---- operator build (K1 + K2), timed separately (mirrors __init__)
+    tb0, tb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tb0.record()
+    op = SparseEmbedding(n, m, cfg["seed"], device=dev, row_range=(r0, r1))
+    tb1.record()
+    torch.cuda.synchronize()
+    build_ms = tb0.elapsed_time(tb1)
+
+    SA = torch.empty((m, d), dtype=sa_dt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def apply_once():
+        if cfg["kind"] == "dense":
+            op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
+        else:
+            op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA)
+
+    def step(kev=None):
+        if kev is not None:
+            kev[0].record(stream)
+        apply_once()
+        if kev is not None:
+            kev[1].record(stream)
+        if world > 1:
+            dist.all_reduce(SA)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def timed_region():
+        kevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        lc0 = launch_count()
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for i in range(args.steps):
+                step(kevs[i])
+            e1.record(stream)
+            torch.cuda.synchronize()
+        launches = launch_count() - lc0
+        if world > 1:
+            dist.barrier()
+        total_ms = e0.elapsed_time(e1)
+        kern_ms = sum(a.elapsed_time(b) for a, b in kevs) / args.steps
+        return total_ms, kern_ms, launches, clk
+
+    total_ms, kern_ms, launches, clk = timed_region()
+    remeasured = False
+    if clk.rejected():
+        log("clock check failed", clk.summary(), "- re-measuring once")
+        total_ms, kern_ms, launches, clk = timed_region()
+        remeasured = True
+
+    # max over ranks
+    t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms_max = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    nnz_total = (n * d) if cfg["kind"] == "dense" else None
+    if nnz_total is None:
+        tt = torch.tensor([nnz_local], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt)
+        nnz_total = int(tt.item())
+    value = nnz_total / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (this rank's apply launch)
+    alg_bytes = in_bytes + m * d * SA.element_size()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    peak, peak_src = peak_hbm()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config),
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
+                "kernel_ms": round(kern_ms, 4), "alg_bytes_per_launch": alg_bytes,
+                "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}
+
+    # ---- end to end through the public API, host buffers
+    e2e = None
+    if not args.no_e2e and cfg["kind"] == "dense":
+        host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+        host.copy_(A)
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        res = op.apply(host, out_dtype=sa_dt)  # warm-up
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            res = op.apply(host, out_dtype=sa_dt)  # H2D + kernel + finiteness check + D2H
+            if world > 1:
+                rt = res.to(dev)
+                dist.all_reduce(rt)
+                res = rt.cpu()
+        e2e_s = torch.tensor([(time.perf_counter() - t0) / e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": nnz_total / float(e2e_s), "unit": "nnz/s",
+               "h2d_bytes_per_step": host.numel() * host.element_size(),
+               "d2h_bytes_per_step": res.numel() * res.element_size(),
+               "steps": e_steps, "ms_per_step": 1e3 * float(e2e_s),
+               "api": "SparseEmbedding.apply(pinned host tensor)"}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg["kind"] == "dense":
+        rows = min(r1 - r0, 1 << 21)
+        cpu = cpu_baseline_sample(args.config, cfg, A[:rows], torch)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded torch generator, BASELINE shapes/distributions)",
+        "config": {"workload": cfg["workload"], "n": n, "d": d, "m": m, "input_dtype": cfg["dtype"],
+                   "sa_dtype": "f32" if sa_dt == torch.float32 else "f64",
+                   "accumulate": "fp64, ascending row order (bit-identical to the reference)",
+                   "l2": "inputs larger than L2 (no flush needed)",
+                   "parallelism": f"row-shard x{world}" + (" + NCCL all-reduce of m x d partials" if world > 1 else "")},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk.summary(), "remeasured": remeasured,
+        "build_ms": round(build_ms, 3), "kernel_ms_max_over_ranks": round(kern_ms_max, 4),
+    }
+    if world > 1:
+        dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)  # W >= 3 warm-up steps
+    cfg = CONFIGS[args.config]
+    line = reference_arm(args, cfg) if args.impl == "reference" else our_arm(args, cfg)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

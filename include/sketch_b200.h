@@ -1,0 +1,150 @@
+/*
+ * sketch_b200.h -- C ABI of the B200-native CountSketch (sparse embedding)
+ * hot path.  Plain pointers and sizes only; every device pointer is caller-
+ * owned (e.g. a torch CUDA tensor's data_ptr), every call is stream-ordered on
+ * the cudaStream_t passed as `stream` (NULL = legacy default stream), and no
+ * call allocates device memory behind the caller's back (workspace queries
+ * give the scratch sizes).  Errors are returned as skt_status; a human-readable
+ * message for the calling thread is available from skt_last_error().
+ *
+ * The reference (/root/reference/pkg/src/sketchnla, pure Python on numpy/scipy)
+ * has no FFI of its own; its drop-in boundary is the duck-typed SketchOperator
+ * protocol (sketch.py:97-119).  Each entry point below replaces one piece of
+ * SparseEmbedding (sketch.py:138-173) or of a caller of it, cited per function.
+ * The Python binding is paper_1207_6365_b200/_lib.py (ctypes); see
+ * INTEGRATION.md for the binding a maintainer adds to sketchnla.
+ */
+#ifndef SKETCH_B200_H
+#define SKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKT_ABI_VERSION 1
+
+typedef enum skt_status {
+  SKT_OK = 0,
+  SKT_EINVAL = 1,    /* bad argument (Python: ValueError, the reference convention) */
+  SKT_ECUDA = 2,     /* CUDA runtime / launch failure (Python: RuntimeError) */
+  SKT_ENOTSUP = 3,   /* valid but unsupported shape/dtype combination */
+  SKT_EWORKSPACE = 4 /* workspace too small */
+} skt_status;
+
+typedef enum skt_dtype { SKT_F32 = 0, SKT_F64 = 1 } skt_dtype;
+typedef enum skt_itype { SKT_I32 = 0, SKT_I64 = 1 } skt_itype;
+
+/* flags for skt_apply_csr */
+#define SKT_CSR_CANONICAL 1u /* no duplicate column inside a row (as_csr output) */
+
+/* 128-bit PCG64 state (numpy's PCG64: state and odd increment), hi/lo words. */
+typedef struct skt_pcg64 {
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} skt_pcg64;
+
+/* ---- host-side utilities ------------------------------------------------ */
+const char *skt_version(void);
+/* Message of the last non-OK status returned on this thread. */
+const char *skt_last_error(void);
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t skt_launch_count(void);
+
+/* numpy.random.SeedSequence(entropy, spawn_key).generate_state(n_out, uint32).
+ * entropy = little-endian 32-bit words of the (non-negative) integer seed.
+ * Replaces the seeding inside sketch.py:51-53 and the derived-seed idiom
+ * SeedSequence(seed, spawn_key=(k,)).generate_state(1)[0] (regress.py:77-78,
+ * leverage.py:72-73, lowrank.py:147-150). */
+skt_status skt_seedseq_generate(const uint32_t *entropy, int32_t n_entropy,
+                                const uint32_t *spawn_key, int32_t n_spawn,
+                                uint32_t *out, int32_t n_out);
+
+/* PCG64(SeedSequence(entropy, spawn_key)) initial state: sketch.py:51-53. */
+skt_status skt_pcg64_seed(const uint32_t *entropy, int32_t n_entropy,
+                          const uint32_t *spawn_key, int32_t n_spawn, skt_pcg64 *out);
+
+/* numpy PCG64.advance(delta): jump ahead delta 64-bit outputs. */
+skt_status skt_pcg64_advance(skt_pcg64 *st, uint64_t delta);
+
+/* ---- K1: bucket hash h and sign s --------------------------------------- */
+/* Replaces sketch.py:147 (bucket = integers(0, t, n)) and sketch.py:148
+ * (sign = choice([-1, 1], n)), bit-exact, for the row range [row_begin,
+ * row_end) of an operator with n >= row_end rows.  h[k] / s[k] receive the
+ * values of row row_begin + k.  1 <= t <= 2^32.  s may be NULL.
+ * When t is not a power of two (Lemire rejection possible), the call
+ * synchronises `stream` once to confirm enough draws were generated. */
+skt_status skt_hash_signs_workspace(int64_t row_end, uint64_t t, size_t *bytes);
+skt_status skt_hash_signs(const skt_pcg64 *bucket_stream, const skt_pcg64 *sign_stream,
+                          int64_t row_begin, int64_t row_end, uint64_t t, uint32_t *h,
+                          int8_t *s, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- K2: the plan (S as a t x n CSR) ------------------------------------ */
+/* Replaces sketch.py:149-151 (csr_array((sign, (bucket, arange(n))))):
+ * indptr[t+1] (int64) = bucket offsets, rows[n] = row ids stably sorted by
+ * bucket (ascending inside a bucket), with the row's sign in bit 31
+ * (1 = -1.0).  n < 2^31. Deterministic (no atomics on the output). */
+skt_status skt_plan_workspace(int64_t n, uint64_t t, size_t *bytes);
+skt_status skt_plan_build(const uint32_t *h, const int8_t *s, int64_t n, uint64_t t,
+                          int64_t *indptr, uint32_t *rows, void *ws, size_t ws_bytes,
+                          void *stream);
+
+/* ---- K3: S.A for dense A ------------------------------------------------ */
+/* Replaces sketch.py:165 (self._mat @ as_dense(a)) and the finiteness scan of
+ * _validation.py:25-26.  A is n x d row-major (leading dim lda, f32 or f64),
+ * SA is t x d row-major (ldsa).  Each SA[b, j] is the fp64 sum over the rows
+ * of bucket b in ascending order starting from +0.0 -- bit-identical to the
+ * reference; sa_dtype = SKT_F32 rounds that fp64 sum once.  If nonfinite_flag
+ * (device int32) is non-NULL it is zeroed and then set to 1 if any entry of A
+ * is Inf/NaN (the caller raises ValueError). */
+skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t,
+                           int64_t n, const void *a, skt_dtype a_dtype, int64_t d,
+                           int64_t lda, void *sa, skt_dtype sa_dtype, int64_t ldsa,
+                           int32_t *nonfinite_flag, void *stream);
+
+/* ---- K4: S.A for CSR A -------------------------------------------------- */
+/* Replaces sketch.py:155-164 (repeat + np.bincount): SA[h(i), j] += s(i) v
+ * for every stored (i, j, v), fp64, per output in ascending row order and
+ * stored order inside a row -- bit-identical to the bincount.  CSR arrays of
+ * A may use int32 or int64 indptr / indices; values f32 or f64.  Without
+ * SKT_CSR_CANONICAL, duplicate columns in a row are handled in stored order. */
+skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64_t t,
+                         int64_t n, const void *a_indptr, skt_itype indptr_type,
+                         const void *a_indices, skt_itype index_type, const void *a_vals,
+                         skt_dtype val_dtype, int64_t d, void *sa, skt_dtype sa_dtype,
+                         int64_t ldsa, uint32_t flags, void *stream);
+
+/* ---- column sketch A.S^T ------------------------------------------------ */
+/* Replaces apply_right (sketch.py:445-448) = (S.apply(A.T)).T without the
+ * transpose: Y[i, h(j)] += s(j) A[i, j], per output ascending j.  A has
+ * n_rows rows and ncols = the operator's n columns; h/s are the operator's
+ * per-column hash and sign (K1 output).  Y is n_rows x t row-major (ldy). */
+skt_status skt_apply_right_dense(const uint32_t *h, const int8_t *s, uint64_t t,
+                                 int64_t n_rows, int64_t ncols, const void *a,
+                                 skt_dtype a_dtype, int64_t lda, void *y, skt_dtype y_dtype,
+                                 int64_t ldy, int32_t *nonfinite_flag, void *stream);
+skt_status skt_apply_right_csr(const uint32_t *h, const int8_t *s, uint64_t t,
+                               int64_t n_rows, int64_t ncols, const void *a_indptr,
+                               skt_itype indptr_type, const void *a_indices,
+                               skt_itype index_type, const void *a_vals, skt_dtype val_dtype,
+                               void *y, skt_dtype y_dtype, int64_t ldy, void *stream);
+
+/* ---- K5: leverage-score contraction ------------------------------------- */
+/* Replaces leverage.py:90-91 (rows = a @ probe; einsum('ij,ij->i', rows, rows))
+ * fused: scores[i] = sum_c (sum_j A[i,j] probe[j,c])^2 with the n x k product
+ * kept on chip.  probe is d x k row-major fp64 (probe = N G^T, leverage.py:89).
+ * fp64 accumulation; scores written as score_dtype. */
+skt_status skt_lev_rownorms_csr(int64_t n, int64_t d, const void *a_indptr,
+                                skt_itype indptr_type, const void *a_indices,
+                                skt_itype index_type, const void *a_vals, skt_dtype val_dtype,
+                                const double *probe, int64_t k, void *scores,
+                                skt_dtype score_dtype, void *stream);
+skt_status skt_lev_rownorms_dense(int64_t n, int64_t d, const void *a, skt_dtype a_dtype,
+                                  int64_t lda, const double *probe, int64_t k, void *scores,
+                                  skt_dtype score_dtype, int32_t *nonfinite_flag, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCH_B200_H */

@@ -1,0 +1,132 @@
+"""ctypes binding of the C ABI in ``include/sketch_b200.h`` (libsketch_b200.so).
+
+This is the one place Python touches native code.  There is no CPU fallback:
+if the shared library is missing or fails to load, or no CUDA device is
+present when a device entry point is called, the call raises.  ctypes releases
+the GIL for the duration of each foreign call, so operators may be applied
+concurrently from several host threads (the reference CLI's ThreadPoolExecutor,
+cli.py:227-231).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsketch_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+SKT_OK, SKT_EINVAL, SKT_ECUDA, SKT_ENOTSUP, SKT_EWORKSPACE = range(5)
+SKT_F32, SKT_F64 = 0, 1
+SKT_I32, SKT_I64 = 0, 1
+SKT_CSR_CANONICAL = 1
+
+# Every symbol include/sketch_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "skt_version",
+    "skt_last_error",
+    "skt_launch_count",
+    "skt_seedseq_generate",
+    "skt_pcg64_seed",
+    "skt_pcg64_advance",
+    "skt_hash_signs_workspace",
+    "skt_hash_signs",
+    "skt_plan_workspace",
+    "skt_plan_build",
+    "skt_apply_dense",
+    "skt_apply_csr",
+    "skt_apply_right_dense",
+    "skt_apply_right_csr",
+    "skt_lev_rownorms_csr",
+    "skt_lev_rownorms_dense",
+)
+
+
+class SktPcg64(ctypes.Structure):
+    _fields_ = [
+        ("state_hi", ctypes.c_uint64),
+        ("state_lo", ctypes.c_uint64),
+        ("inc_hi", ctypes.c_uint64),
+        ("inc_lo", ctypes.c_uint64),
+    ]
+
+
+class SketchError(RuntimeError):
+    """CUDA / unsupported-shape failure reported by the native library."""
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libsketch_b200.so for sm_100a in-tree (nvcc via make)."""
+    cmd = ["make", "-C", CSRC, "-j8"]
+    out = subprocess.run(cmd, capture_output=not verbose, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"building libsketch_b200.so failed:\n{out.stdout}\n{out.stderr}")
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u32, u64, sz = (
+        ctypes.c_void_p,
+        ctypes.c_int32,
+        ctypes.c_int64,
+        ctypes.c_uint32,
+        ctypes.c_uint64,
+        ctypes.c_size_t,
+    )
+    PS = ctypes.POINTER(SktPcg64)
+    sig = {
+        "skt_version": ([], ctypes.c_char_p),
+        "skt_last_error": ([], ctypes.c_char_p),
+        "skt_launch_count": ([], u64),
+        "skt_seedseq_generate": ([P, i32, P, i32, P, i32], i32),
+        "skt_pcg64_seed": ([P, i32, P, i32, PS], i32),
+        "skt_pcg64_advance": ([PS, u64], i32),
+        "skt_hash_signs_workspace": ([i64, u64, ctypes.POINTER(sz)], i32),
+        "skt_hash_signs": ([PS, PS, i64, i64, u64, P, P, P, sz, P], i32),
+        "skt_plan_workspace": ([i64, u64, ctypes.POINTER(sz)], i32),
+        "skt_plan_build": ([P, P, i64, u64, P, P, P, sz, P], i32),
+        "skt_apply_dense": ([P, P, u64, i64, P, i32, i64, i64, P, i32, i64, P, P], i32),
+        "skt_apply_csr": ([P, P, u64, i64, P, i32, P, i32, P, i32, i64, P, i32, i64, u32, P], i32),
+        "skt_apply_right_dense": ([P, P, u64, i64, i64, P, i32, i64, P, i32, i64, P, P], i32),
+        "skt_apply_right_csr": ([P, P, u64, i64, i64, P, i32, P, i32, P, i32, P, i32, i64, P], i32),
+        "skt_lev_rownorms_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, P], i32),
+        "skt_lev_rownorms_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, P, P], i32),
+    }
+    for name, (argtypes, restype) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = argtypes
+        fn.restype = restype
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    msg = lib().skt_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int) -> None:
+    if status == SKT_OK:
+        return
+    msg = last_error()
+    if status == SKT_EINVAL:
+        raise ValueError(msg)
+    raise SketchError(f"status {status}: {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().skt_launch_count())

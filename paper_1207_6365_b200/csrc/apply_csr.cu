@@ -1,0 +1,183 @@
+// apply_csr.cu -- K4: SA = S.A for CSR A (reference sketch.py:155-164: repeat
+// + np.bincount, i.e. out[h(i)*d + j] += s(i) * v over the stored nonzeros in
+// row-major order, fp64 from +0.0).
+//
+// One warp owns one bucket and keeps its SA row as d fp64 accumulators in
+// shared memory.  The bucket's rows are taken 32 at a time from the plan
+// (ascending row id); their nonzeros are first staged into shared memory with
+// coalesced, flattened loads (every lane has many loads in flight), then
+// accumulated row by row in plan order.  Inside a row the columns are distinct
+// (canonical CSR), so one warp step adds up to 32 of them without conflicts;
+// successive rows are ordered by __syncwarp.  Per output element the additions
+// therefore happen in ascending row order, exactly as the bincount does --
+// bit-identical fp64.  Non-canonical rows (duplicate columns) are serialised
+// in stored order with __match_any_sync.
+#include "common.cuh"
+
+namespace skt {
+namespace {
+
+constexpr int kStage = 256;  // staged nonzeros per warp per window
+constexpr int kMaxWarps = 8;
+
+struct WarpSmem {
+  // byte offsets inside one warp's slice
+  static __host__ __device__ size_t acc_bytes(int64_t d) { return ((size_t)d * 8 + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t bytes(int64_t d) {
+    return acc_bytes(d) + kStage * 8 + kStage * 4 + 34 * 4 + 32 * 8;
+  }
+};
+
+template <typename I>
+__device__ __forceinline__ int64_t ld_idx(const I *p) {
+  return (int64_t)__ldg(p);
+}
+
+template <typename IP, typename IX, typename TV, typename TOut, bool kCanon>
+__global__ void __launch_bounds__(kMaxWarps * 32) apply_csr_kernel(
+    const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
+    const IP *__restrict__ aip, const IX *__restrict__ aix, const TV *__restrict__ av, int64_t d,
+    TOut *__restrict__ sa, int64_t ldsa) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t bucket = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (bucket >= (int64_t)t) return;  // whole warp exits together
+
+  unsigned char *base = smem_raw + (size_t)w * WarpSmem::bytes(d);
+  double *acc = (double *)base;
+  double *sval = (double *)(base + WarpSmem::acc_bytes(d));
+  int32_t *scol = (int32_t *)(sval + kStage);
+  int32_t *soff = scol + kStage;             // 33 used
+  int64_t *srs = (int64_t *)(soff + 34);     // 32 row starts, sign in bit 63
+
+  for (int64_t c = lane; c < d; c += 32) acc[c] = 0.0;
+  const int64_t beg = pindptr[bucket], end = pindptr[bucket + 1];
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  for (int64_t k0 = beg; k0 < end; k0 += 32) {
+    const int nrows = (int)((end - k0) < 32 ? (end - k0) : 32);
+    const bool valid = lane < nrows;
+    const uint32_t wrd = valid ? __ldg(prow + k0 + lane) : 0u;
+    const int64_t row = wrd & 0x7fffffffu;
+    const int64_t rs = valid ? ld_idx(aip + row) : 0;
+    const int64_t re = valid ? ld_idx(aip + row + 1) : 0;
+    const int32_t len = (int32_t)(re - rs);
+    // exclusive scan of row lengths
+    int32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t off = incl - len;
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    soff[lane] = off;
+    if (lane == 31) soff[32] = total;
+    srs[lane] = rs | ((int64_t)(wrd >> 31) << 63);
+    __syncwarp();
+
+    for (int32_t w0 = 0; w0 < total; w0 += kStage) {
+      const int32_t wend = min(total, w0 + kStage);
+      // ---- stage: flattened, coalesced loads of this window's nonzeros
+      for (int32_t f = w0 + lane; f < wend; f += 32) {
+        int lo = 0, hi = nrows;  // find r: soff[r] <= f < soff[r+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (soff[mid] <= f) lo = mid; else hi = mid;
+        }
+        const int64_t rsw = srs[lo];
+        const int64_t p = (rsw & 0x7fffffffffffffffLL) + (f - soff[lo]);
+        const double v = (double)av[p];
+        scol[f - w0] = (int32_t)aix[p];
+        sval[f - w0] = rsw < 0 ? -v : v;
+      }
+      __syncwarp();
+      // ---- accumulate in plan (= ascending row) order
+      for (int r = 0; r < nrows; ++r) {
+        const int32_t pb = max(soff[r], w0), pe = min(soff[r + 1], wend);
+        for (int32_t p0 = pb; p0 < pe; p0 += 32) {
+          const int32_t p = p0 + lane;
+          const bool has = p < pe;
+          const int32_t c = has ? scol[p - w0] : -1;
+          const double v = has ? sval[p - w0] : 0.0;
+          if (kCanon) {
+            if (has) acc[c] += v;
+          } else {
+            const uint32_t peers = __match_any_sync(0xffffffffu, c);
+            const int rank = __popc(peers & lt_mask);
+            const int rounds = __reduce_max_sync(0xffffffffu, has ? rank + 1 : 0);
+            for (int rr = 0; rr < rounds; ++rr) {
+              if (has && rank == rr) acc[c] += v;
+              __syncwarp();
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  TOut *o = sa + bucket * ldsa;
+  for (int64_t c = lane; c < d; c += 32) o[c] = (TOut)acc[c];
+}
+
+template <typename IP, typename IX, typename TV, typename TOut>
+skt_status launch(const int64_t *pindptr, const uint32_t *prow, uint64_t t, const void *aip,
+                  const void *aix, const void *av, int64_t d, void *sa, int64_t ldsa, bool canon,
+                  cudaStream_t stream) {
+  const size_t per_warp = WarpSmem::bytes(d);
+  const size_t kSmemMax = 200 * 1024;
+  int warps = (int)std::min<size_t>(kMaxWarps, kSmemMax / per_warp);
+  if (warps < 1) return fail(SKT_ENOTSUP, "skt_apply_csr", "d too wide for the shared-memory accumulator");
+  const size_t smem = per_warp * warps;
+  const int64_t blocks = ((int64_t)t + warps - 1) / warps;
+  auto k = canon ? apply_csr_kernel<IP, IX, TV, TOut, true> : apply_csr_kernel<IP, IX, TV, TOut, false>;
+  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_csr");
+  SKT_LAUNCH(k, (unsigned)blocks, warps * 32, smem, stream, pindptr, prow, t, (const IP *)aip,
+             (const IX *)aix, (const TV *)av, d, (TOut *)sa, ldsa);
+  return check_launch("skt_apply_csr");
+}
+
+template <typename IP, typename IX>
+skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, uint64_t t, const void *aip,
+                   const void *aix, const void *av, skt_dtype vt, int64_t d, void *sa,
+                   skt_dtype ot, int64_t ldsa, bool canon, cudaStream_t s) {
+  if (vt == SKT_F32)
+    return ot == SKT_F64 ? launch<IP, IX, float, double>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s)
+                         : launch<IP, IX, float, float>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s);
+  return ot == SKT_F64 ? launch<IP, IX, double, double>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s)
+                       : launch<IP, IX, double, float>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s);
+}
+
+}  // namespace
+}  // namespace skt
+
+using namespace skt;
+
+extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64_t t,
+                                    int64_t n, const void *a_indptr, skt_itype indptr_type,
+                                    const void *a_indices, skt_itype index_type,
+                                    const void *a_vals, skt_dtype val_dtype, int64_t d, void *sa,
+                                    skt_dtype sa_dtype, int64_t ldsa, uint32_t flags,
+                                    void *stream_) {
+  static const char *fn = "skt_apply_csr";
+  if (!indptr || t < 1 || t > (1ull << 32) || n < 0 || d < 0 || ldsa < d || !a_indptr ||
+      (indptr_type != SKT_I32 && indptr_type != SKT_I64) ||
+      (index_type != SKT_I32 && index_type != SKT_I64) ||
+      (val_dtype != SKT_F32 && val_dtype != SKT_F64) ||
+      (sa_dtype != SKT_F32 && sa_dtype != SKT_F64) || d >= (1LL << 31))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  if (d == 0) return SKT_OK;
+  if (!sa || (n > 0 && !rows)) return fail(SKT_EINVAL, fn, "NULL buffer");
+  cudaStream_t s = as_stream(stream_);
+  const bool canon = (flags & SKT_CSR_CANONICAL) != 0;
+  if (indptr_type == SKT_I32)
+    return index_type == SKT_I32
+               ? by_vals<int32_t, int32_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s)
+               : by_vals<int32_t, int64_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s);
+  return index_type == SKT_I32
+             ? by_vals<int64_t, int32_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s)
+             : by_vals<int64_t, int64_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s);
+}

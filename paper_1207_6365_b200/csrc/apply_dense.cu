@@ -1,0 +1,210 @@
+// apply_dense.cu -- K3: SA = S.A for dense row-major A (reference sketch.py:165,
+// scipy csr_matvecs over the t x n plan, after as_dense's finiteness scan
+// _validation.py:16-27).
+//
+// Work item = (bucket b, column chunk).  A group of G lanes (G | 32) owns one
+// work item; lane g of the group owns VEC consecutive columns and keeps VEC
+// fp64 accumulators in registers.  The group walks the bucket's rows in plan
+// order (ascending row id) and adds s_i * A[i, cols] sequentially from +0.0,
+// i.e. exactly the reference's per-element accumulation order, so the fp64
+// result is bit-identical.  Rows are gathered with 128-bit non-allocating
+// loads, kUnroll rows in flight per lane before the ordered accumulation.
+// The non-finite check of as_dense is fused (exponent-all-ones test).
+#include "common.cuh"
+
+namespace skt {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T, int VEC>
+struct Vec;
+template <>
+struct Vec<float, 4> {
+  using type = float4;
+};
+template <>
+struct Vec<float, 2> {
+  using type = float2;
+};
+template <>
+struct Vec<float, 1> {
+  using type = float;
+};
+template <>
+struct Vec<double, 2> {
+  using type = double2;
+};
+template <>
+struct Vec<double, 1> {
+  using type = double;
+};
+
+__device__ __forceinline__ float4 ldstream(const float4 *p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ldstream(const float2 *p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldstream(const float *p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ldstream(const double2 *p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldstream(const double *p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ bool nonfinite(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
+}
+__device__ __forceinline__ bool nonfinite(double x) {
+  return ((uint32_t)(__double_as_longlong(x) >> 32) & 0x7ff00000u) == 0x7ff00000u;
+}
+
+template <typename TIn, typename TOut, int VEC, int G, int kUnroll>
+__global__ void __launch_bounds__(kThreads) apply_dense_kernel(
+    const int64_t *__restrict__ indptr, const uint32_t *__restrict__ rows, int64_t n_items,
+    int64_t n_chunks, const TIn *__restrict__ a, int64_t d, int64_t lda, TOut *__restrict__ sa,
+    int64_t ldsa, int32_t *__restrict__ flag) {
+  using V = typename Vec<TIn, VEC>::type;
+  constexpr int kGroups = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G, glane = lane % G;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t item = warp * kGroups + grp;
+  const bool live = item < n_items;
+  const int64_t bucket = live ? item / n_chunks : 0;
+  const int64_t chunk = live ? item % n_chunks : 0;
+  const int64_t col = chunk * (int64_t)(G * VEC) + (int64_t)glane * VEC;
+  const bool active = live && col < d;
+
+  double acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = 0.0;
+  bool bad = false;
+
+  const int64_t beg = live ? indptr[bucket] : 0;
+  const int64_t end = live ? indptr[bucket + 1] : 0;
+  const TIn *acol = a + col;
+  for (int64_t k0 = beg; k0 < end; k0 += kUnroll) {
+    uint32_t w[kUnroll];
+    V v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) w[u] = (k0 + u < end) ? __ldg(rows + k0 + u) : 0u;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (active && k0 + u < end)
+        v[u] = ldstream(reinterpret_cast<const V *>(acol + (int64_t)(w[u] & 0x7fffffffu) * lda));
+      else
+        v[u] = V{};
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k0 + u < end) {
+        const bool neg = (w[u] >> 31) != 0;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const TIn x = reinterpret_cast<const TIn *>(&v[u])[k];
+          bad |= nonfinite(x);
+          const double xd = (double)x;
+          acc[k] += neg ? -xd : xd;
+        }
+      }
+    }
+  }
+  if (active) {
+    TOut *o = sa + bucket * ldsa + col;
+    if (col + VEC <= d) {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) o[k] = (TOut)acc[k];
+    } else {
+      for (int k = 0; k < VEC && col + k < d; ++k) o[k] = (TOut)acc[k];
+    }
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+template <typename TIn, typename TOut, int VEC, int G>
+skt_status launch(const int64_t *indptr, const uint32_t *rows, uint64_t t, const TIn *a,
+                  int64_t d, int64_t lda, TOut *sa, int64_t ldsa, int32_t *flag,
+                  cudaStream_t stream) {
+  const int64_t n_chunks = (d + G * VEC - 1) / (G * VEC);
+  const int64_t n_items = (int64_t)t * n_chunks;
+  const int64_t warps = (n_items + (32 / G) - 1) / (32 / G);
+  const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  constexpr int kUnroll = (sizeof(TIn) * VEC >= 16) ? 8 : 16;
+  SKT_LAUNCH((apply_dense_kernel<TIn, TOut, VEC, G, kUnroll>), (unsigned)blocks, kThreads, 0, stream,
+             indptr, rows, n_items, n_chunks, a, d, lda, sa, ldsa, flag);
+  return check_launch("skt_apply_dense");
+}
+
+template <typename TIn, typename TOut, int VEC>
+skt_status dispatch_g(const int64_t *indptr, const uint32_t *rows, uint64_t t, const TIn *a,
+                      int64_t d, int64_t lda, TOut *sa, int64_t ldsa, int32_t *flag,
+                      cudaStream_t stream) {
+  const int64_t lanes = (d + VEC - 1) / VEC;
+  if (lanes <= 1) return launch<TIn, TOut, VEC, 1>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  if (lanes <= 2) return launch<TIn, TOut, VEC, 2>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  if (lanes <= 4) return launch<TIn, TOut, VEC, 4>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  if (lanes <= 8) return launch<TIn, TOut, VEC, 8>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  if (lanes <= 16) return launch<TIn, TOut, VEC, 16>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  return launch<TIn, TOut, VEC, 32>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+}
+
+template <typename TIn, typename TOut>
+skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a_,
+                        int64_t d, int64_t lda, void *sa_, int64_t ldsa, int32_t *flag,
+                        cudaStream_t stream) {
+  const TIn *a = (const TIn *)a_;
+  TOut *sa = (TOut *)sa_;
+  const uintptr_t ap = (uintptr_t)a;
+  auto ok = [&](int vec) {
+    return d % vec == 0 && lda % vec == 0 && ap % (sizeof(TIn) * vec) == 0;
+  };
+  if (sizeof(TIn) == 4 && ok(4))
+    return dispatch_g<TIn, TOut, (sizeof(TIn) == 4 ? 4 : 2)>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  if (ok(2)) return dispatch_g<TIn, TOut, 2>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+  return dispatch_g<TIn, TOut, 1>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
+}
+
+}  // namespace
+}  // namespace skt
+
+using namespace skt;
+
+extern "C" skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t,
+                                      int64_t n, const void *a, skt_dtype a_dtype, int64_t d,
+                                      int64_t lda, void *sa, skt_dtype sa_dtype, int64_t ldsa,
+                                      int32_t *nonfinite_flag, void *stream_) {
+  static const char *fn = "skt_apply_dense";
+  if (!indptr || t < 1 || t > (1ull << 32) || n < 0 || d < 0 || lda < d || ldsa < d ||
+      (a_dtype != SKT_F32 && a_dtype != SKT_F64) || (sa_dtype != SKT_F32 && sa_dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  cudaStream_t stream = as_stream(stream_);
+  if (nonfinite_flag) SKT_CUDA_TRY(cudaMemsetAsync(nonfinite_flag, 0, sizeof(int32_t), stream), fn);
+  if (d == 0) return SKT_OK;
+  if (!sa || (n > 0 && (!a || !rows))) return fail(SKT_EINVAL, fn, "NULL buffer");
+  if (a_dtype == SKT_F32)
+    return sa_dtype == SKT_F64
+               ? dispatch_vec<float, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream)
+               : dispatch_vec<float, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream);
+  return sa_dtype == SKT_F64
+             ? dispatch_vec<double, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream)
+             : dispatch_vec<double, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream);
+}

@@ -1,0 +1,207 @@
+// lev.cu -- K5: leverage-score contraction (reference leverage.py:87-91):
+//   rows = A @ probe   (probe = N G^T, d x k)      scores_i = sum_c rows_ic^2
+// fused: A is streamed once, the n x k product never touches HBM, only the n
+// scores are written.
+//
+// This file holds the fp64 CUDA-core path (used for fp64 A, and as the
+// exact-accumulation path for fp32 A): one warp per row, lane c owns probe
+// column c (k > 32 loops over column chunks), the probe lives in shared memory
+// as fp64, nonzeros are fetched 32 at a time and broadcast with shuffles, the
+// next row's nonzeros are prefetched while the current row is contracted.
+// Per (row, column) the products are accumulated in stored-nonzero order with
+// fp64 FMA; the 32-lane square-sum uses a fixed butterfly (deterministic).
+#include "common.cuh"
+
+namespace skt {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr size_t kProbeSmemMax = 96 * 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <bool kSmemProbe>
+__device__ __forceinline__ double probe_at(const double *sp, const double *gp, int64_t idx) {
+  return kSmemProbe ? sp[idx] : __ldg(gp + idx);
+}
+
+template <typename IP, typename IX, typename TV, typename TS, bool kSmemProbe>
+__global__ void __launch_bounds__(kThreads) lev_csr_kernel(
+    int64_t n, int64_t d, const IP *__restrict__ aip, const IX *__restrict__ aix,
+    const TV *__restrict__ av, const double *__restrict__ probe, int64_t k,
+    TS *__restrict__ scores) {
+  extern __shared__ __align__(16) double sprobe[];
+  if (kSmemProbe) {
+    for (int64_t i = threadIdx.x; i < d * k; i += blockDim.x) sprobe[i] = probe[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  for (int64_t row = warp; row < n; row += nwarps) {
+    const int64_t rs = (int64_t)aip[row], re = (int64_t)aip[row + 1];
+    double score = 0.0;
+    for (int64_t c0 = 0; c0 < k; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const bool cl = c < k;
+      double acc = 0.0;
+      for (int64_t p0 = rs; p0 < re; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const bool has = p < re;
+        const int32_t j = has ? (int32_t)aix[p] : 0;
+        const double v = has ? (double)av[p] : 0.0;
+        const int cnt = (int)min((int64_t)32, re - p0);
+        for (int q = 0; q < cnt; ++q) {
+          const int32_t jq = __shfl_sync(0xffffffffu, j, q);
+          const double vq = __shfl_sync(0xffffffffu, v, q);
+          if (cl) acc = fma(vq, probe_at<kSmemProbe>(sprobe, probe, (int64_t)jq * k + c), acc);
+        }
+      }
+      score += warp_sum(cl ? acc * acc : 0.0);
+    }
+    if (lane == 0) scores[row] = (TS)score;
+  }
+}
+
+template <typename TA, typename TS, bool kSmemProbe>
+__global__ void __launch_bounds__(kThreads) lev_dense_kernel(int64_t n, int64_t d,
+                                                             const TA *__restrict__ a, int64_t lda,
+                                                             const double *__restrict__ probe,
+                                                             int64_t k, TS *__restrict__ scores,
+                                                             int32_t *__restrict__ flag) {
+  extern __shared__ __align__(16) double sprobe[];
+  if (kSmemProbe) {
+    for (int64_t i = threadIdx.x; i < d * k; i += blockDim.x) sprobe[i] = probe[i];
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  bool bad = false;
+  for (int64_t row = warp; row < n; row += nwarps) {
+    const TA *ar = a + row * lda;
+    double score = 0.0;
+    for (int64_t c0 = 0; c0 < k; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const bool cl = c < k;
+      double acc = 0.0;
+      for (int64_t j0 = 0; j0 < d; j0 += 32) {
+        const bool has = j0 + lane < d;
+        const double v = has ? (double)ar[j0 + lane] : 0.0;
+        if (c0 == 0) bad |= !isfinite(v);
+        const int cnt = (int)min((int64_t)32, d - j0);
+        for (int q = 0; q < cnt; ++q) {
+          const double vq = __shfl_sync(0xffffffffu, v, q);
+          if (cl) acc = fma(vq, probe_at<kSmemProbe>(sprobe, probe, (j0 + q) * k + c), acc);
+        }
+      }
+      score += warp_sum(cl ? acc * acc : 0.0);
+    }
+    if (lane == 0) scores[row] = (TS)score;
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+inline int64_t grid_for(int64_t n) {
+  const int64_t want = (n + kWarps - 1) / kWarps;
+  return std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * 8));
+}
+
+template <typename IP, typename IX, typename TV, typename TS>
+skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, const void *av,
+                      const double *p, int64_t k, void *scores, cudaStream_t st) {
+  static const char *fn = "skt_lev_rownorms_csr";
+  const size_t pbytes = (size_t)d * k * sizeof(double);
+  const int64_t blocks = grid_for(n);
+  if (pbytes <= kProbeSmemMax) {
+    auto kern = lev_csr_kernel<IP, IX, TV, TS, true>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes), fn);
+    SKT_LAUNCH(kern, (unsigned)blocks, kThreads, pbytes, st, n, d, (const IP *)aip, (const IX *)aix,
+               (const TV *)av, p, k, (TS *)scores);
+  } else {
+    SKT_LAUNCH((lev_csr_kernel<IP, IX, TV, TS, false>), (unsigned)blocks, kThreads, 0, st, n, d,
+               (const IP *)aip, (const IX *)aix, (const TV *)av, p, k, (TS *)scores);
+  }
+  return check_launch(fn);
+}
+
+template <typename IP, typename IX>
+skt_status csr_types(int64_t n, int64_t d, const void *aip, const void *aix, const void *av,
+                     skt_dtype vt, const double *p, int64_t k, void *scores, skt_dtype st_,
+                     cudaStream_t st) {
+  if (vt == SKT_F32)
+    return st_ == SKT_F64 ? launch_csr<IP, IX, float, double>(n, d, aip, aix, av, p, k, scores, st)
+                          : launch_csr<IP, IX, float, float>(n, d, aip, aix, av, p, k, scores, st);
+  return st_ == SKT_F64 ? launch_csr<IP, IX, double, double>(n, d, aip, aix, av, p, k, scores, st)
+                        : launch_csr<IP, IX, double, float>(n, d, aip, aix, av, p, k, scores, st);
+}
+
+template <typename TA, typename TS>
+skt_status launch_dense(int64_t n, int64_t d, const void *a, int64_t lda, const double *p,
+                        int64_t k, void *scores, int32_t *flag, cudaStream_t st) {
+  static const char *fn = "skt_lev_rownorms_dense";
+  const size_t pbytes = (size_t)d * k * sizeof(double);
+  const int64_t blocks = grid_for(n);
+  if (pbytes <= kProbeSmemMax) {
+    auto kern = lev_dense_kernel<TA, TS, true>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes), fn);
+    SKT_LAUNCH(kern, (unsigned)blocks, kThreads, pbytes, st, n, d, (const TA *)a, lda, p, k,
+               (TS *)scores, flag);
+  } else {
+    SKT_LAUNCH((lev_dense_kernel<TA, TS, false>), (unsigned)blocks, kThreads, 0, st, n, d,
+               (const TA *)a, lda, p, k, (TS *)scores, flag);
+  }
+  return check_launch(fn);
+}
+
+}  // namespace
+}  // namespace skt
+
+using namespace skt;
+
+extern "C" skt_status skt_lev_rownorms_csr(int64_t n, int64_t d, const void *a_indptr,
+                                           skt_itype indptr_type, const void *a_indices,
+                                           skt_itype index_type, const void *a_vals,
+                                           skt_dtype val_dtype, const double *probe, int64_t k,
+                                           void *scores, skt_dtype score_dtype, void *stream_) {
+  static const char *fn = "skt_lev_rownorms_csr";
+  if (n < 0 || d < 0 || k < 0 || !a_indptr || (indptr_type != SKT_I32 && indptr_type != SKT_I64) ||
+      (index_type != SKT_I32 && index_type != SKT_I64) ||
+      (val_dtype != SKT_F32 && val_dtype != SKT_F64) ||
+      (score_dtype != SKT_F32 && score_dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  if (n == 0) return SKT_OK;
+  if (!scores || (k > 0 && d > 0 && !probe)) return fail(SKT_EINVAL, fn, "NULL buffer");
+  cudaStream_t st = as_stream(stream_);
+  if (indptr_type == SKT_I32)
+    return index_type == SKT_I32
+               ? csr_types<int32_t, int32_t>(n, d, a_indptr, a_indices, a_vals, val_dtype, probe, k, scores, score_dtype, st)
+               : csr_types<int32_t, int64_t>(n, d, a_indptr, a_indices, a_vals, val_dtype, probe, k, scores, score_dtype, st);
+  return index_type == SKT_I32
+             ? csr_types<int64_t, int32_t>(n, d, a_indptr, a_indices, a_vals, val_dtype, probe, k, scores, score_dtype, st)
+             : csr_types<int64_t, int64_t>(n, d, a_indptr, a_indices, a_vals, val_dtype, probe, k, scores, score_dtype, st);
+}
+
+extern "C" skt_status skt_lev_rownorms_dense(int64_t n, int64_t d, const void *a, skt_dtype a_dtype,
+                                             int64_t lda, const double *probe, int64_t k,
+                                             void *scores, skt_dtype score_dtype,
+                                             int32_t *nonfinite_flag, void *stream_) {
+  static const char *fn = "skt_lev_rownorms_dense";
+  if (n < 0 || d < 0 || k < 0 || lda < d || (a_dtype != SKT_F32 && a_dtype != SKT_F64) ||
+      (score_dtype != SKT_F32 && score_dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  cudaStream_t st = as_stream(stream_);
+  if (nonfinite_flag) SKT_CUDA_TRY(cudaMemsetAsync(nonfinite_flag, 0, sizeof(int32_t), st), fn);
+  if (n == 0) return SKT_OK;
+  if (!scores || (d > 0 && !a) || (k > 0 && d > 0 && !probe)) return fail(SKT_EINVAL, fn, "NULL buffer");
+  if (a_dtype == SKT_F32)
+    return score_dtype == SKT_F64 ? launch_dense<float, double>(n, d, a, lda, probe, k, scores, nonfinite_flag, st)
+                                  : launch_dense<float, float>(n, d, a, lda, probe, k, scores, nonfinite_flag, st);
+  return score_dtype == SKT_F64 ? launch_dense<double, double>(n, d, a, lda, probe, k, scores, nonfinite_flag, st)
+                                : launch_dense<double, float>(n, d, a, lda, probe, k, scores, nonfinite_flag, st);
+}

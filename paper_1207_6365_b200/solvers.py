@@ -1,0 +1,262 @@
+"""Callers of the hot path, mirroring the reference's entry points.
+
+* ``sketch_solve_ls``  -- regress.py:85-116: two GPU sketch applies (A, b), the
+  thin SVD-pseudoinverse solve of (SA, Sb) on the host (linalg.py:75-90, the
+  reference's own LAPACK path, so x is bit-identical when SA is), and the
+  residual on the original data recomputed on the GPU.
+* ``lev_rownorms``     -- leverage.py:90-91 fused on the GPU (K5).
+* ``leverage_scores_sketched`` -- the config-4 pipeline of leverage.py:74-91
+  with an explicit sketch size and probe width: S.A (GPU) -> pivoted QR /
+  basis change (host, leverage.py:36-47) -> probe = N G^T -> scores (GPU).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from ._lib import check
+from .sketch import (
+    SparseEmbedding,
+    _ITYPE,
+    _TORCH_TO_SKT,
+    _ptr,
+    _stream_ptr,
+    check_eps,
+    default_sparse_dim,
+    seed_words,
+    sparse_embedding_or_identity,
+)
+
+RANK_REL_TOL = 1e-10  # linalg.py:20-32 Tolerances.rank_rel_tol
+
+
+def as_dense(a, name: str = "matrix") -> np.ndarray:
+    """_validation.py:16-27."""
+    if sp.issparse(a):
+        a = a.toarray()
+    out = np.asarray(a, dtype=np.float64)
+    if out.ndim == 1:
+        out = out.reshape(-1, 1)
+    if out.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {out.shape}")
+    if not np.all(np.isfinite(out)):
+        raise ValueError(f"{name} contains non-finite entries")
+    return out
+
+
+def as_csr(a, name: str = "matrix") -> sp.csr_array:
+    """_validation.py:30-41."""
+    out = sp.csr_array(a, dtype=np.float64) if sp.issparse(a) else sp.csr_array(as_dense(a, name))
+    out.sum_duplicates()
+    out.eliminate_zeros()
+    out.sort_indices()
+    if not np.all(np.isfinite(out.data)):
+        raise ValueError(f"{name} contains non-finite entries")
+    return out
+
+
+def as_matrix(a, name: str = "matrix"):
+    return as_csr(a, name) if sp.issparse(a) else as_dense(a, name)
+
+
+def pseudoinverse_solve(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """linalg.py:75-90 (thin SVD, singular values below 1e-10 sigma_1 dropped)."""
+    u, sigma, vt = np.linalg.svd(a, full_matrices=False)
+    if sigma.size == 0 or sigma[0] == 0.0:
+        return np.zeros((a.shape[1], b.shape[1]))
+    rank = int(np.count_nonzero(sigma > RANK_REL_TOL * sigma[0]))
+    if rank == 0:
+        return np.zeros((a.shape[1], b.shape[1]))
+    ur, sr, vr = u[:, :rank], sigma[:rank], vt.T[:, :rank]
+    return vr @ ((ur.T @ b) / sr[:, None])
+
+
+@dataclass(frozen=True)
+class RegressionSolution:
+    """regress.py:54-64 (fields used by sketch_solve_ls)."""
+
+    x: np.ndarray
+    residual_norm: float
+    method: str
+    sketch_dim: int
+    seed: int
+    iterations: int = 0
+    residual_history: tuple = ()
+    coreset: object = None
+
+
+def _residual_fro_gpu(a, x: np.ndarray, b: np.ndarray, device) -> float:
+    """||A x - b||_F on the device (regress.py:81-82)."""
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to(device)
+    bt = torch.from_numpy(np.ascontiguousarray(b)).to(device)
+    if sp.issparse(a):
+        m = sp.csr_array(a)
+        at = torch.sparse_csr_tensor(
+            torch.from_numpy(m.indptr.astype(np.int64)).to(device),
+            torch.from_numpy(m.indices.astype(np.int64)).to(device),
+            torch.from_numpy(m.data.astype(np.float64)).to(device),
+            size=m.shape,
+        )
+        r = at @ xt - bt
+    else:
+        at = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
+        r = at @ xt - bt
+    return float(torch.linalg.norm(r).item())
+
+
+def sketch_solve_ls(a, b, eps: float, seed: int = 0, operator=None) -> RegressionSolution:
+    """regress.py:85-116 with the sketch applied on the GPU."""
+    a = as_matrix(a)
+    b = as_dense(b)
+    if a.shape[0] != b.shape[0]:
+        raise ValueError(f"operands must have the same number of rows: {a.shape[0]} vs {b.shape[0]}")
+    eps = check_eps(eps)
+    if operator is None:
+        t = default_sparse_dim(a.shape[1] + b.shape[1], eps)
+        operator = sparse_embedding_or_identity(a.shape[0], t, seed)
+    sa = operator.apply(a)
+    sb = operator.apply(b)
+    x = pseudoinverse_solve(np.asarray(sa), np.asarray(sb))
+    device = getattr(operator, "device", None) or torch.device("cuda", torch.cuda.current_device())
+    return RegressionSolution(
+        x=x,
+        residual_norm=_residual_fro_gpu(a, x, b, device),
+        method="sketch",
+        sketch_dim=operator.output_dim,
+        seed=int(seed),
+    )
+
+
+# ---------------------------------------------------------------------------
+# leverage scores
+# ---------------------------------------------------------------------------
+def pivoted_qr_rank(a: np.ndarray):
+    """linalg.py:142-155."""
+    q, r, perm = scipy.linalg.qr(a, mode="economic", pivoting=True)
+    diag = np.abs(np.diag(r))
+    rank = 0 if diag.size == 0 or diag[0] == 0.0 else int(np.count_nonzero(diag > RANK_REL_TOL * diag[0]))
+    return q, r, perm, rank
+
+
+def basis_change(sketched: np.ndarray):
+    """leverage.py:36-47: N (d x rank) with sketched @ N orthonormal."""
+    _, r, perm, rank = pivoted_qr_rank(sketched)
+    if rank == 0:
+        return np.zeros((sketched.shape[1], 0)), 0
+    n_mat = np.zeros((sketched.shape[1], rank))
+    n_mat[perm[:rank]] = np.linalg.inv(r[:rank, :rank])
+    return n_mat, rank
+
+
+def gaussian_jl_entries(rows: int, cols: int, seed: int) -> np.ndarray:
+    """GaussianJl.entries (sketch.py:344-355): _rng(seed, 4, 0) normals / sqrt(rows)."""
+    rng = np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(4, 0)))
+    return rng.standard_normal((rows, cols)) / math.sqrt(rows)
+
+
+def lev_rownorms(a, probe, device=None, out_dtype=torch.float64):
+    """scores_i = ||A_i probe||^2 (leverage.py:90-91) fused on the GPU (K5).
+
+    ``a``: scipy CSR / numpy dense / torch (CUDA) dense or sparse-CSR tensor;
+    ``probe``: d x k (fp64).  Returns numpy for host input, torch otherwise.
+    """
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    L = _lib.lib()
+    host = not isinstance(a, torch.Tensor)
+    p = torch.as_tensor(np.ascontiguousarray(probe, dtype=np.float64) if not isinstance(probe, torch.Tensor) else probe)
+    p = p.to(device=device, dtype=torch.float64).contiguous()
+    d, k = p.shape
+    with torch.cuda.device(device):
+        stream = _stream_ptr(device)
+        if sp.issparse(a) or (isinstance(a, torch.Tensor) and a.layout == torch.sparse_csr):
+            if isinstance(a, torch.Tensor):
+                ip, ix, vv = (x.to(device) for x in (a.crow_indices(), a.col_indices(), a.values()))
+                n = a.shape[0]
+            else:
+                m = sp.csr_array(a)
+                if m.data.dtype not in (np.float32, np.float64):
+                    m = sp.csr_array(m, dtype=np.float64)
+                n = m.shape[0]
+                ip, ix, vv = (torch.from_numpy(np.ascontiguousarray(x)).to(device) for x in (m.indptr, m.indices, m.data))
+            if a.shape[1] != d:
+                raise ValueError(f"probe has {d} rows, matrix has {a.shape[1]} columns")
+            if vv.dtype not in _TORCH_TO_SKT:
+                vv = vv.to(torch.float64)
+            out = torch.empty(n, dtype=out_dtype, device=device)
+            check(
+                L.skt_lev_rownorms_csr(
+                    n, d, _ptr(ip), _ITYPE[ip.dtype], _ptr(ix), _ITYPE[ix.dtype], _ptr(vv),
+                    _TORCH_TO_SKT[vv.dtype], _ptr(p), k, _ptr(out), _TORCH_TO_SKT[out_dtype], stream,
+                )
+            )
+        else:
+            x = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(a)))
+            x = x.to(device)
+            if x.dtype not in _TORCH_TO_SKT:
+                x = x.to(torch.float64)
+            x = x.reshape(x.shape[0], -1).contiguous()
+            if x.shape[1] != d:
+                raise ValueError(f"probe has {d} rows, matrix has {x.shape[1]} columns")
+            out = torch.empty(x.shape[0], dtype=out_dtype, device=device)
+            flag = torch.empty(1, dtype=torch.int32, device=device)
+            check(
+                L.skt_lev_rownorms_dense(
+                    x.shape[0], d, _ptr(x), _TORCH_TO_SKT[x.dtype], max(d, 1), _ptr(p), k, _ptr(out),
+                    _TORCH_TO_SKT[out_dtype], _ptr(flag), stream,
+                )
+            )
+            if x.shape[0] > 0 and int(flag.item()) != 0:
+                raise ValueError("matrix contains non-finite entries")
+    if host:
+        return out.cpu().numpy()
+    return out if a.is_cuda else out.cpu()
+
+
+@dataclass(frozen=True)
+class LeverageRun:
+    scores: np.ndarray
+    rank: int
+    sa: np.ndarray
+    probe: np.ndarray
+
+
+def leverage_scores_sketched(a, m: int, k: int, seed: int, rep: int = 0) -> LeverageRun:
+    """One repetition of leverage.py:71-91 with sketch size ``m`` and JL width
+    ``k`` chosen by the caller (the SRHT stage is the identity when m does not
+    exceed _srht_rows(rank), as in BASELINE config 4)."""
+    sub = np.random.SeedSequence(int(seed), spawn_key=(100 + rep,)).generate_state(3)
+    n = a.shape[0]
+    s = SparseEmbedding(n, m, int(sub[0]))
+    sa = s.apply(a)
+    n_mat, rank = basis_change(sa)
+    if rank == 0:
+        return LeverageRun(np.zeros(n), 0, sa, np.zeros((a.shape[1], 0)))
+    g = gaussian_jl_entries(k, rank, int(sub[2]))
+    probe = n_mat @ g.T
+    scores = lev_rownorms(a, probe)
+    return LeverageRun(scores, rank, sa, probe)
+
+
+__all__ = [
+    "as_dense",
+    "as_csr",
+    "as_matrix",
+    "pseudoinverse_solve",
+    "RegressionSolution",
+    "sketch_solve_ls",
+    "pivoted_qr_rank",
+    "basis_change",
+    "gaussian_jl_entries",
+    "lev_rownorms",
+    "leverage_scores_sketched",
+    "seed_words",
+]

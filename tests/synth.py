@@ -1,0 +1,63 @@
+"""Seeded synthetic inputs with BASELINE.json's shapes and value distributions
+(numpy default_rng; regenerated bit-identically on the GPU box from the seeds).
+
+No public dataset is named by BASELINE.json; the paper's UF-collection corpus
+is not in this container and is not recreated.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+SKETCH_SEED = 1  # SparseEmbedding(n, m, seed=1) as in BASELINE.md's CPU baseline
+
+
+def csr_fixed_nnz(rng, n: int, d: int, per_row: int, dtype=np.float64, scale: float = 1.0):
+    """n x d CSR with exactly `per_row` distinct uniform columns per row (sorted),
+    values N(0, scale^2)."""
+    cols = np.empty((n, per_row), dtype=np.int32)
+    chunk = 1 << 17
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        keys = rng.random((r1 - r0, d))
+        cols[r0:r1] = np.sort(np.argpartition(keys, per_row - 1, axis=1)[:, :per_row], axis=1)
+    vals = (scale * rng.standard_normal(n * per_row)).astype(dtype)
+    indptr = np.arange(0, (n + 1) * per_row, per_row, dtype=np.int64)
+    if indptr[-1] < 2**31:
+        indptr = indptr.astype(np.int32)
+    return sp.csr_array((vals, cols.ravel(), indptr), shape=(n, d))
+
+
+def config1():
+    """C1: dense fp64 100,000 x 20 ~ N(0,1); b = A x* + 0.1 N(0,1); m = 4,000."""
+    rng = np.random.default_rng(101)
+    a = rng.standard_normal((100_000, 20))
+    x = rng.standard_normal((20, 1))
+    b = a @ x + 0.1 * rng.standard_normal((100_000, 1))
+    return a, b, SKETCH_SEED
+
+
+def config2():
+    """C2: CSR fp64 1e6 x 50, exactly 5 distinct uniform columns per row, N(0,1);
+    b = A x* + 0.01 N(0,1); m = 25,000."""
+    rng = np.random.default_rng(102)
+    a = csr_fixed_nnz(rng, 1_000_000, 50, 5)
+    x = rng.standard_normal((50, 1))
+    b = np.asarray(a @ x) + 0.01 * rng.standard_normal((1_000_000, 1))
+    return a, b, SKETCH_SEED
+
+
+def lev_case():
+    """Config-4 shaped leverage case, scaled to oracle size: CSR fp64 n=20,000,
+    d=16, 6 random columns per row, 1% of rows fully dense with N(0, 100)
+    values; sketch m = 2,000; JL probe k = 32."""
+    rng = np.random.default_rng(104)
+    n, d = 20_000, 16
+    a = csr_fixed_nnz(rng, n, d, 6).tolil()
+    dense_rows = rng.choice(n, size=n // 100, replace=False)
+    for r in dense_rows:
+        a[r, :] = 10.0 * rng.standard_normal(d)
+    a = sp.csr_array(a)
+    a.sort_indices()
+    return a, 2_000, 32, 7

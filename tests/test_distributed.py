@@ -1,0 +1,84 @@
+"""N > 1 path on CPU: world_size-2 gloo ranks run the row sharding and the
+all-reduce of partial SA; the per-shard partial is computed by the oracle (the
+GPU kernel's role), the result must equal the single-process reference SA to
+1e-12 (reassociation across shards)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1207_6365_b200.distributed import ShardedSparseEmbedding, shard_rows
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_rows_cover_disjoint():
+    for n in (1, 7, 100, 16_777_216):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_rows(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    with pytest.raises(ValueError):
+        shard_rows(10, 2, 2)
+
+
+def _worker(rank, world, port, n, t, d, seed, kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        import scipy.sparse as sp
+
+        rng = np.random.default_rng(123)
+        h, s = O.hash_signs(n, t, seed)
+        if kind == "dense":
+            a = rng.standard_normal((n, d))
+        else:
+            a = sp.csr_array(sp.random_array((n, d), density=0.2, rng=rng, format="csr"))
+
+        def partial(a_local, out_dtype):
+            r0, r1 = op.row_begin, op.row_end
+            if kind == "dense":
+                p = O.apply_dense(h[r0:r1], s[r0:r1], t, a_local)
+            else:
+                p = O.apply_csr(h[r0:r1], s[r0:r1], t, a_local)
+            return torch.from_numpy(p).to(out_dtype)
+
+        op = ShardedSparseEmbedding(n, t, seed, partial_fn=partial)
+        local = a[op.row_begin : op.row_end]
+        out = op.apply(local).numpy()
+        if rank == 0:
+            full = O.apply(h, s, t, a)
+            rel = np.linalg.norm(out - full) / max(np.linalg.norm(full), 1e-300)
+            q.put((rel, op.row_begin, op.row_end))
+        with pytest.raises(ValueError):
+            op.apply(a[:1] if op.row_end - op.row_begin != 1 else a[:2])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_two_rank_gloo_allreduce_matches_reference(kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n, t, d, seed = 5_001, 97, 6, 3
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, t, d, seed, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    rel, r0, r1 = q.get(timeout=10)
+    assert (r0, r1) == (0, 2500)
+    assert rel <= 1e-12

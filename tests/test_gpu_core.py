@@ -1,0 +1,287 @@
+"""GPU parity: K1 (h/s), K2 (plan), K3/K4 (S.A), column sketch, K5 against the
+oracle and the reference's golden outputs.  Bit-exact for h, s, plan and fp64
+S.A; tolerances are stated where the arithmetic differs."""
+
+import ctypes
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+from oracle import oracle as O
+from paper_1207_6365_b200 import SparseEmbedding, apply_right, make_sparse_embedding
+from paper_1207_6365_b200 import _lib
+from paper_1207_6365_b200.sketch import pcg64_state
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+def gpu_hash(n, t, seed, r0=0, r1=None):
+    r1 = n if r1 is None else r1
+    L = _lib.lib()
+    hs, ss = pcg64_state(seed, (0, 0)), pcg64_state(seed, (0, 1))
+    h = torch.empty(r1 - r0, dtype=torch.int32, device="cuda")
+    s = torch.empty(r1 - r0, dtype=torch.int8, device="cuda")
+    nb = ctypes.c_size_t()
+    _lib.check(L.skt_hash_signs_workspace(r1, t, ctypes.byref(nb)))
+    ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device="cuda")
+    _lib.check(L.skt_hash_signs(ctypes.byref(hs), ctypes.byref(ss), r0, r1, t, h.data_ptr(), s.data_ptr(),
+                                ws.data_ptr(), nb.value, torch.cuda.current_stream().cuda_stream))
+    return h.cpu().numpy().view(np.uint32), s.cpu().numpy()
+
+
+# ---------------------------------------------------------------- K1
+def test_hash_signs_golden():
+    z = load("hash_cases.npz")
+    meta = json.load(open(os.path.join(GOLDEN, "hash_cases.json")))
+    for k, (n, t, seed) in enumerate(meta):
+        h, s = gpu_hash(n, t, seed)
+        assert np.array_equal(h, z[f"h{k}"]), (n, t, seed)
+        assert np.array_equal(s, z[f"s{k}"]), (n, t, seed)
+
+
+@pytest.mark.parametrize("t", [4000, 65536, 3 * 2**30, 2**31 + 1, 7])
+def test_hash_signs_row_ranges(t):
+    n = 50_001
+    h_full, s_full = O.hash_signs(n, t, 3)
+    for r0, r1 in [(0, 1), (1, 2), (17, 4111), (4096, 50_001), (25_000, 25_001), (0, n)]:
+        h, s = gpu_hash(n, t, 3, r0, r1)
+        assert np.array_equal(h, h_full[r0:r1]), (r0, r1)
+        assert np.array_equal(s, s_full[r0:r1]), (r0, r1)
+
+
+def test_hash_signs_config_sizes():
+    """Full-size h/s for configs 1-5 (n up to 16.8M) against the C oracle."""
+    for n, t in [(100_000, 4000), (1_000_000, 25_000), (16_777_216, 65_536), (4_194_304, 16_384), (262_144, 400)]:
+        h, s = gpu_hash(n, t, 1)
+        ho, so = O.hash_signs(n, t, 1)
+        assert np.array_equal(h, ho) and np.array_equal(s, so), (n, t)
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))
+    for c in ("config1", "config2"):
+        h, s = gpu_hash(cfg[c]["n"], cfg[c]["t"], cfg[c]["seed"])
+        assert sha(h) == cfg[c]["sha_h"] and sha(s) == cfg[c]["sha_s"]
+
+
+# ---------------------------------------------------------------- K2
+@pytest.mark.parametrize("n,t", [(1, 1), (64, 1), (5, 7), (1000, 2), (4097, 255), (4096, 256), (20_000, 257),
+                                 (100_000, 4000), (1_000_000, 25_000), (300_000, 2**20 + 7), (5000, 3 * 2**30)])
+def test_plan_matches_stable_counting_sort(n, t):
+    op = SparseEmbedding(n, t, seed=n + t)
+    h, s = O.hash_signs(n, t, n + t)
+    indptr, rows = O.plan(h, t)
+    got_rows = op.plan_rows.cpu().numpy().view(np.uint32)
+    assert np.array_equal(op.plan_indptr.cpu().numpy(), indptr)
+    assert np.array_equal((got_rows & 0x7FFFFFFF).astype(np.int32), rows)
+    assert np.array_equal((got_rows >> 31).astype(bool), s[rows] < 0)
+
+
+def test_host_views_match_reference_layout():
+    op = make_sparse_embedding(9, 5, seed=1)
+    h, s = O.hash_signs(9, 5, 1)
+    assert np.array_equal(op.bucket, h.astype(np.int64)) and op.bucket.dtype == np.int64
+    assert np.array_equal(op.sign, s.astype(np.float64))
+    ref = sp.csr_array((s.astype(np.float64), (h.astype(np.int64), np.arange(9))), shape=(5, 9))
+    assert np.array_equal(op._mat.toarray(), ref.toarray()) and op._mat.nnz == 9
+
+
+# ---------------------------------------------------------------- K3 / K4
+def _golden_cases():
+    return [m for m in json.load(open(os.path.join(GOLDEN, "apply_cases.json"))) if m["kind"] != "right"]
+
+
+@pytest.mark.parametrize("case", _golden_cases(), ids=lambda m: m["name"])
+def test_apply_golden_bit_exact(case):
+    z = load("apply_cases.npz")
+    name = case["name"]
+    op = SparseEmbedding(case["n"], case["t"], case["seed"])
+    if case["kind"] == "csr":
+        a = sp.csr_array((z[f"{name}_data"], z[f"{name}_indices"], z[f"{name}_indptr"]),
+                         shape=tuple(z[f"{name}_shape"]))
+    else:
+        a = z[f"{name}_a"]
+    got = op.apply(a)
+    assert got.dtype == np.float64
+    assert np.array_equal(got, z[f"{name}_sa"]), name
+    # torch CUDA input path, same bits
+    if case["kind"] == "dense":
+        gt = op.apply(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+        assert np.array_equal(gt.cpu().numpy().reshape(got.shape), got)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 20, 33, 64, 128, 130, 257])
+def test_apply_dense_shapes(dtype, d, rng):
+    n, t = 3000, 211
+    a = rng.standard_normal((n, d)).astype(dtype)
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    ref = O.apply_dense(h, s, t, a)
+    assert np.array_equal(op.apply(a), ref)
+    f32 = op.apply(torch.from_numpy(a).cuda(), out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(f32, ref.astype(np.float32))  # one rounding of the exact fp64 sum
+
+
+def test_apply_dense_strided_rows(rng):
+    n, t = 1000, 37
+    big = torch.from_numpy(rng.standard_normal((n, 40))).cuda()
+    view = big[:, 3:19]  # lda = 40, misaligned start
+    op = SparseEmbedding(n, t, seed=4)
+    h, s = O.hash_signs(n, t, 4)
+    assert np.array_equal(op.apply(view).cpu().numpy(), O.apply_dense(h, s, t, view.cpu().numpy()))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d,density", [(1, 0.5), (50, 0.1), (64, 0.25), (300, 0.02), (2000, 0.005)])
+def test_apply_csr_shapes(dtype, d, density, rng):
+    n, t = 5000, 97
+    a = sp.csr_array(sp.random_array((n, d), density=density, rng=rng, format="csr"), dtype=dtype)
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    ref = O.np_apply_csr(h, s, t, a)
+    assert np.array_equal(op.apply(a), ref)
+    a64 = sp.csr_array((a.data, a.indices.astype(np.int64), a.indptr.astype(np.int64)), shape=a.shape)
+    assert np.array_equal(op.apply(a64), ref)
+
+
+def test_apply_csr_long_rows_and_duplicates(rng):
+    # rows longer than the staging window and non-canonical duplicates
+    n, d, t = 300, 5000, 11
+    dense = rng.standard_normal((n, d)) * (rng.random((n, d)) < 0.6)
+    a = sp.csr_array(dense)
+    op = SparseEmbedding(n, t, seed=9)
+    h, s = O.hash_signs(n, t, 9)
+    assert np.array_equal(op.apply(a), O.np_apply_csr(h, s, t, a))
+    rows = np.repeat(np.arange(50), 40)
+    cols = rng.integers(0, 7, size=rows.size)
+    vals = rng.standard_normal(rows.size)
+    dup = sp.csr_array((vals, cols, np.arange(0, rows.size + 1, 40)), shape=(50, 7))
+    assert not dup.has_canonical_format
+    op2 = SparseEmbedding(50, 3, seed=2)
+    h2, s2 = O.hash_signs(50, 3, 2)
+    assert np.array_equal(op2.apply(dup), O.np_apply_csr(h2, s2, 3, dup))
+
+
+def test_apply_torch_sparse_csr(rng):
+    n, d, t = 4000, 64, 300
+    a = sp.csr_array(sp.random_array((n, d), density=0.2, rng=rng, format="csr"), dtype=np.float32)
+    ta = torch.sparse_csr_tensor(torch.from_numpy(a.indptr.astype(np.int64)), torch.from_numpy(a.indices.astype(np.int64)),
+                                 torch.from_numpy(a.data), size=a.shape).cuda()
+    op = SparseEmbedding(n, t, seed=1)
+    h, s = O.hash_signs(n, t, 1)
+    assert np.array_equal(op.apply(ta).cpu().numpy(), O.np_apply_csr(h, s, t, a))
+
+
+def test_nonfinite_and_shape_errors(rng):
+    op = SparseEmbedding(10, 4, seed=0)
+    a = rng.standard_normal((10, 3))
+    for bad in (np.nan, np.inf, -np.inf):
+        b = a.copy()
+        b[7, 2] = bad
+        with pytest.raises(ValueError):
+            op.apply(b)
+        with pytest.raises(ValueError):
+            op.apply(torch.from_numpy(b.astype(np.float32)).cuda())
+    with pytest.raises(ValueError):
+        op.apply(rng.standard_normal((11, 2)))
+    with pytest.raises(ValueError):
+        SparseEmbedding(4, 0, seed=0)
+    with pytest.raises(ValueError):
+        SparseEmbedding(0, 4, seed=0)
+
+
+# ---- the reference's own hot-path properties (test_sketch.py:37-84, 231-273)
+def test_unit_vector_maps_to_signed_basis():
+    op = make_sparse_embedding(5, 7, seed=3)
+    for j in range(5):
+        e = np.zeros((5, 1))
+        e[j] = 1.0
+        out = op.apply(e).ravel()
+        assert np.count_nonzero(out) == 1 and out[op.bucket[j]] == op.sign[j]
+
+
+def test_structure_zero_linearity_determinism(rng):
+    op = make_sparse_embedding(9, 5, seed=1)
+    dense = op.dense()
+    assert all(np.count_nonzero(dense[:, j]) == 1 and abs(dense[:, j]).max() == 1.0 for j in range(9))
+    assert np.all(make_sparse_embedding(4, 8, seed=0).apply(np.zeros((4, 1))) == 0)
+    op = make_sparse_embedding(20, 9, seed=3)
+    a, b = rng.standard_normal((20, 4)), rng.standard_normal((20, 4))
+    assert np.abs(op.apply(a + b) - op.apply(a) - op.apply(b)).max() <= 1e-12
+    x, y = (make_sparse_embedding(30, 10, seed=5) for _ in range(2))
+    assert np.array_equal(x.bucket, y.bucket) and np.array_equal(x.sign, y.sign)
+    dense = rng.standard_normal((30, 5)) * (rng.random((30, 5)) < 0.4)
+    op = make_sparse_embedding(30, 11, seed=1)
+    assert np.array_equal(op.apply(dense), op.apply(sp.csr_array(dense)))
+
+
+def test_monte_carlo_unbiased():
+    x = np.ones((4, 1))
+    total = sum(float(np.sum(make_sparse_embedding(4, 8, seed=seed).apply(x) ** 2)) for seed in range(2000))
+    assert 3.8 <= total / 2000 <= 4.2
+
+
+# ---------------------------------------------------------------- column sketch
+def test_apply_right_golden():
+    z = load("apply_cases.npz")
+    op = SparseEmbedding(60, 9, 13)
+    assert np.array_equal(apply_right(z["right_dense_a"], op), z["right_dense_y"])
+    ac = sp.csr_array((z["right_csr_data"], z["right_csr_indices"], z["right_csr_indptr"]), shape=(25, 60))
+    assert np.array_equal(apply_right(ac, op), z["right_csr_y"])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_apply_right_matches_transpose_formula(dtype, rng):
+    n_cols, t = 3000, 150
+    op = SparseEmbedding(n_cols, t, seed=8)
+    h, s = O.hash_signs(n_cols, t, 8)
+    a = rng.standard_normal((40, n_cols)).astype(dtype)
+    ref = O.apply_dense(h, s, t, np.ascontiguousarray(a.T)).T
+    assert np.array_equal(apply_right(a, op), ref)
+    ac = sp.csr_array(sp.random_array((40, n_cols), density=0.05, rng=rng, format="csr"), dtype=dtype)
+    ref2 = O.np_apply_csr(h, s, t, sp.csr_array(ac.T)).T
+    assert np.array_equal(apply_right(ac, op), ref2)
+
+
+# ---------------------------------------------------------------- K5
+def test_lev_rownorms_golden():
+    from paper_1207_6365_b200.solvers import lev_rownorms
+    from tests import synth
+
+    z = load("lev_case.npz")
+    a, m, k, seed = synth.lev_case()
+    got = lev_rownorms(a, z["probe"])
+    assert np.max(np.abs(got - z["scores"]) / np.abs(z["scores"])) <= 1e-12
+    a32 = sp.csr_array(a, dtype=np.float32)
+    ref32 = O.lev_rownorms_csr(a32, z["probe"])
+    got32 = lev_rownorms(a32, z["probe"], out_dtype=torch.float32)
+    assert np.max(np.abs(got32 - ref32) / ref32) <= 1e-5
+    gd = lev_rownorms(a.toarray(), z["probe"])
+    assert np.max(np.abs(gd - z["scores"]) / np.abs(z["scores"])) <= 1e-12
+
+
+def test_leverage_pipeline_matches_reference_pieces():
+    from paper_1207_6365_b200.solvers import leverage_scores_sketched
+    from tests import synth
+
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))["lev"]
+    z = load("lev_case.npz")
+    a, m, k, seed = synth.lev_case()
+    run = leverage_scores_sketched(a, m, k, seed)
+    assert sha(run.sa) == cfg["sha_sa"]  # GPU S.A bit-identical to the reference
+    assert run.rank == cfg["rank"]
+    assert sha(run.probe) == cfg["sha_probe"]
+    assert np.max(np.abs(run.scores - z["scores"]) / np.abs(z["scores"])) <= 1e-12
