@@ -81,14 +81,19 @@ skt_status skt_hash_signs(const skt_pcg64 *bucket_stream, const skt_pcg64 *sign_
                           int8_t *s, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- K2: the plan (S as a t x n CSR) ------------------------------------ */
-/* Replaces sketch.py:149-151 (csr_array((sign, (bucket, arange(n))))):
- * indptr[t+1] (int64) = bucket offsets, rows[n] = row ids stably sorted by
- * bucket (ascending inside a bucket), with the row's sign in bit 31
- * (1 = -1.0).  n < 2^31. Deterministic (no atomics on the output). */
-skt_status skt_plan_workspace(int64_t n, uint64_t t, size_t *bytes);
+/* Replaces sketch.py:149-151 (csr_array((sign, (bucket, arange(n))))).
+ * shift = 0: indptr[t+1] (int64) = bucket offsets, rows[n] = row ids stably
+ * sorted by bucket (ascending inside a bucket) -- exactly _mat.indptr /
+ * _mat.indices -- with the row's sign in bit 31 (1 = -1.0).
+ * shift = k in 1..8: the same rows stably sorted by bucket GROUP h >> k
+ * (groups of 2^k consecutive buckets, ascending row order inside a group);
+ * indptr has ngroups+1 = ((t-1) >> k) + 2 entries and blo[n] (uint8) gets each
+ * row's bucket inside its group.  This is the order the grouped S.A kernels
+ * sweep.  n < 2^31.  Deterministic (no atomics on positions). */
+skt_status skt_plan_workspace(int64_t n, uint64_t t, int32_t shift, size_t *bytes);
 skt_status skt_plan_build(const uint32_t *h, const int8_t *s, int64_t n, uint64_t t,
-                          int64_t *indptr, uint32_t *rows, void *ws, size_t ws_bytes,
-                          void *stream);
+                          int32_t shift, int64_t *indptr, uint32_t *rows, uint8_t *blo,
+                          void *ws, size_t ws_bytes, void *stream);
 
 /* ---- K3: S.A for dense A ------------------------------------------------ */
 /* Replaces sketch.py:165 (self._mat @ as_dense(a)) and the finiteness scan of
@@ -106,14 +111,18 @@ skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t
 /* ---- K4: S.A for CSR A -------------------------------------------------- */
 /* Replaces sketch.py:155-164 (repeat + np.bincount): SA[h(i), j] += s(i) v
  * for every stored (i, j, v), fp64, per output in ascending row order and
- * stored order inside a row -- bit-identical to the bincount.  CSR arrays of
- * A may use int32 or int64 indptr / indices; values f32 or f64.  Without
- * SKT_CSR_CANONICAL, duplicate columns in a row are handled in stored order. */
-skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64_t t,
-                         int64_t n, const void *a_indptr, skt_itype indptr_type,
-                         const void *a_indices, skt_itype index_type, const void *a_vals,
-                         skt_dtype val_dtype, int64_t d, void *sa, skt_dtype sa_dtype,
-                         int64_t ldsa, uint32_t flags, void *stream);
+ * stored order inside a row -- bit-identical to the bincount.  (indptr, rows,
+ * blo, shift) is a plan from skt_plan_build; canonical input (flag
+ * SKT_CSR_CANONICAL: no duplicate column inside a row) with narrow d runs the
+ * grouped sweep kernel for any shift, otherwise a shift-0 plan is required.
+ * CSR arrays of A may use int32 or int64 indptr / indices; values f32 or f64;
+ * nnz = number of stored entries (a_indptr[n]). */
+skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, const uint8_t *blo,
+                         int32_t shift, uint64_t t, int64_t n, const void *a_indptr,
+                         skt_itype indptr_type, const void *a_indices, skt_itype index_type,
+                         const void *a_vals, skt_dtype val_dtype, int64_t nnz, int64_t d,
+                         void *sa, skt_dtype sa_dtype, int64_t ldsa, uint32_t flags,
+                         void *stream);
 
 /* ---- column sketch A.S^T ------------------------------------------------ */
 /* Replaces apply_right (sketch.py:445-448) = (S.apply(A.T)).T without the

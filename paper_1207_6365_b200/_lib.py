@@ -97,10 +97,10 @@ def lib() -> ctypes.CDLL:
         "skt_pcg64_advance": ([PS, u64], i32),
         "skt_hash_signs_workspace": ([i64, u64, ctypes.POINTER(sz)], i32),
         "skt_hash_signs": ([PS, PS, i64, i64, u64, P, P, P, sz, P], i32),
-        "skt_plan_workspace": ([i64, u64, ctypes.POINTER(sz)], i32),
-        "skt_plan_build": ([P, P, i64, u64, P, P, P, sz, P], i32),
+        "skt_plan_workspace": ([i64, u64, i32, ctypes.POINTER(sz)], i32),
+        "skt_plan_build": ([P, P, i64, u64, i32, P, P, P, P, sz, P], i32),
         "skt_apply_dense": ([P, P, u64, i64, P, i32, i64, i64, P, i32, i64, P, P], i32),
-        "skt_apply_csr": ([P, P, u64, i64, P, i32, P, i32, P, i32, i64, P, i32, i64, u32, P], i32),
+        "skt_apply_csr": ([P, P, P, i32, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, u32, P], i32),
         "skt_apply_right_dense": ([P, P, u64, i64, i64, P, i32, i64, P, i32, i64, P, P], i32),
         "skt_apply_right_csr": ([P, P, u64, i64, i64, P, i32, P, i32, P, i32, P, i32, i64, P], i32),
         "skt_lev_rownorms_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, P], i32),

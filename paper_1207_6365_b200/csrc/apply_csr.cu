@@ -12,7 +12,12 @@
 // therefore happen in ascending row order, exactly as the bincount does --
 // bit-identical fp64.  Non-canonical rows (duplicate columns) are serialised
 // in stored order with __match_any_sync.
+#include <type_traits>
+
 #include "common.cuh"
+#include "csr_group.cuh"
+#include "csr_lane.cuh"
+#include "csr_tile.cuh"
 
 namespace skt {
 namespace {
@@ -124,31 +129,73 @@ __global__ void __launch_bounds__(kMaxWarps * 32) apply_csr_kernel(
 }
 
 template <typename IP, typename IX, typename TV, typename TOut>
-skt_status launch(const int64_t *pindptr, const uint32_t *prow, uint64_t t, const void *aip,
-                  const void *aix, const void *av, int64_t d, void *sa, int64_t ldsa, bool canon,
-                  cudaStream_t stream) {
+skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
+                  uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
+                  int64_t nnz, int64_t d, void *sa, int64_t ldsa, bool canon, cudaStream_t stream) {
+  static const char *fn = "skt_apply_csr";
+  const int64_t gb = 1LL << shift;
+  const bool short_rows = n > 0 && nnz <= 8 * n;  // mean row length <= 8
+  // (1) grouped sweep over a bucket-group plan (short rows)
+  const size_t group_acc = (size_t)gb * d * sizeof(double);
+  if (canon && shift > 0 && group_acc <= 24 * 1024) {
+    const int64_t ngroups = (int64_t)((t - 1) >> shift) + 1;
+    const size_t smem = group_acc * kGroupWarps;
+    const int64_t blocks = (ngroups + kGroupWarps - 1) / kGroupWarps;
+    auto k = short_rows ? csr_group_kernel<IP, IX, TV, TOut, 8> : csr_group_kernel<IP, IX, TV, TOut, 16>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+    SKT_LAUNCH(k, (unsigned)blocks, kGroupWarps * 32, smem, stream, pindptr, prow, blo, ngroups,
+               shift, t, (const IP *)aip, (const IX *)aix, (const TV *)av, (int)d, (TOut *)sa, ldsa);
+    return check_launch(fn);
+  }
+  // (2) densify-in-shared-memory tiles, warp per bucket (longer rows)
+  if (canon && shift == 0 && d <= kTileMaxD) {
+    const int dp = (int)((d + 1) & ~1LL);
+    const int R = (int)std::min<int64_t>(32, tile_bytes<TV>() / ((int64_t)dp * sizeof(TV)));
+    const size_t smem = (size_t)(tile_bytes<TV>() + 32 * sizeof(int4)) * kTileWarps;
+    const int64_t blocks = ((int64_t)t + kTileWarps - 1) / kTileWarps;
+    const int chunks = (int)((d + 63) / 64);
+    auto k = chunks <= 1 ? csr_tile_kernel<IP, IX, TV, TOut, 1>
+                         : chunks <= 2 ? csr_tile_kernel<IP, IX, TV, TOut, 2> : csr_tile_kernel<IP, IX, TV, TOut, 4>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+    SKT_LAUNCH(k, (unsigned)blocks, kTileWarps * 32, smem, stream, pindptr, prow, t, (const IP *)aip,
+               (const IX *)aix, (const TV *)av, (int)d, dp, R, (TOut *)sa, ldsa);
+    return check_launch(fn);
+  }
+  // (3) bucket-lane kernel: one bucket per lane (moderate d)
+  const size_t lane_smem = short_rows ? LaneSmem<IX, TV, 8>::bytes((int)d) : LaneSmem<IX, TV, 16>::bytes((int)d);
+  if (canon && shift == 0 && lane_smem <= 200 * 1024) {
+    const int64_t blocks = ((int64_t)t + 31) / 32;
+    auto k = short_rows ? csr_lane_kernel<IP, IX, TV, TOut, 8> : csr_lane_kernel<IP, IX, TV, TOut, 16>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lane_smem), fn);
+    SKT_LAUNCH(k, (unsigned)blocks, 32, lane_smem, stream, pindptr, prow, t, (const IP *)aip,
+               (const IX *)aix, (const TV *)av, (int)d, (TOut *)sa, ldsa);
+    return check_launch(fn);
+  }
+  if (shift != 0)
+    return fail(SKT_EINVAL, fn, "non-canonical or wide-d CSR needs the per-bucket plan (shift 0)");
   const size_t per_warp = WarpSmem::bytes(d);
   const size_t kSmemMax = 200 * 1024;
   int warps = (int)std::min<size_t>(kMaxWarps, kSmemMax / per_warp);
-  if (warps < 1) return fail(SKT_ENOTSUP, "skt_apply_csr", "d too wide for the shared-memory accumulator");
+  if (warps < 1) return fail(SKT_ENOTSUP, fn, "d too wide for the shared-memory accumulator");
   const size_t smem = per_warp * warps;
   const int64_t blocks = ((int64_t)t + warps - 1) / warps;
   auto k = canon ? apply_csr_kernel<IP, IX, TV, TOut, true> : apply_csr_kernel<IP, IX, TV, TOut, false>;
-  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_csr");
+  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
   SKT_LAUNCH(k, (unsigned)blocks, warps * 32, smem, stream, pindptr, prow, t, (const IP *)aip,
              (const IX *)aix, (const TV *)av, d, (TOut *)sa, ldsa);
-  return check_launch("skt_apply_csr");
+  return check_launch(fn);
 }
 
 template <typename IP, typename IX>
-skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, uint64_t t, const void *aip,
-                   const void *aix, const void *av, skt_dtype vt, int64_t d, void *sa,
-                   skt_dtype ot, int64_t ldsa, bool canon, cudaStream_t s) {
+skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
+                   uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
+                   skt_dtype vt, int64_t nnz, int64_t d, void *sa, skt_dtype ot, int64_t ldsa,
+                   bool canon, cudaStream_t s) {
   if (vt == SKT_F32)
-    return ot == SKT_F64 ? launch<IP, IX, float, double>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s)
-                         : launch<IP, IX, float, float>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s);
-  return ot == SKT_F64 ? launch<IP, IX, double, double>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s)
-                       : launch<IP, IX, double, float>(pindptr, prow, t, aip, aix, av, d, sa, ldsa, canon, s);
+    return ot == SKT_F64 ? launch<IP, IX, float, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s)
+                         : launch<IP, IX, float, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s);
+  return ot == SKT_F64 ? launch<IP, IX, double, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s)
+                       : launch<IP, IX, double, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s);
 }
 
 }  // namespace
@@ -156,18 +203,20 @@ skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, uint64_t t, con
 
 using namespace skt;
 
-extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64_t t,
-                                    int64_t n, const void *a_indptr, skt_itype indptr_type,
+extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows,
+                                    const uint8_t *blo, int32_t shift, uint64_t t, int64_t n,
+                                    const void *a_indptr, skt_itype indptr_type,
                                     const void *a_indices, skt_itype index_type,
-                                    const void *a_vals, skt_dtype val_dtype, int64_t d, void *sa,
-                                    skt_dtype sa_dtype, int64_t ldsa, uint32_t flags,
-                                    void *stream_) {
+                                    const void *a_vals, skt_dtype val_dtype, int64_t nnz,
+                                    int64_t d, void *sa, skt_dtype sa_dtype, int64_t ldsa,
+                                    uint32_t flags, void *stream_) {
   static const char *fn = "skt_apply_csr";
   if (!indptr || t < 1 || t > (1ull << 32) || n < 0 || d < 0 || ldsa < d || !a_indptr ||
+      shift < 0 || shift > 8 || (shift > 0 && n > 0 && !blo) ||
       (indptr_type != SKT_I32 && indptr_type != SKT_I64) ||
       (index_type != SKT_I32 && index_type != SKT_I64) ||
       (val_dtype != SKT_F32 && val_dtype != SKT_F64) ||
-      (sa_dtype != SKT_F32 && sa_dtype != SKT_F64) || d >= (1LL << 31))
+      (sa_dtype != SKT_F32 && sa_dtype != SKT_F64) || d >= (1LL << 31) || nnz < 0)
     return fail(SKT_EINVAL, fn, "bad arguments");
   if (d == 0) return SKT_OK;
   if (!sa || (n > 0 && !rows)) return fail(SKT_EINVAL, fn, "NULL buffer");
@@ -175,9 +224,9 @@ extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows,
   const bool canon = (flags & SKT_CSR_CANONICAL) != 0;
   if (indptr_type == SKT_I32)
     return index_type == SKT_I32
-               ? by_vals<int32_t, int32_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s)
-               : by_vals<int32_t, int64_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s);
+               ? by_vals<int32_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s)
+               : by_vals<int32_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s);
   return index_type == SKT_I32
-             ? by_vals<int64_t, int32_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s)
-             : by_vals<int64_t, int64_t>(indptr, rows, t, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, canon, s);
+             ? by_vals<int64_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s)
+             : by_vals<int64_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s);
 }

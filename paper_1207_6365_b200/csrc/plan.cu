@@ -1,5 +1,8 @@
 // plan.cu -- K2: the sketch plan = S as a t x n CSR (reference sketch.py:149-151,
-// scipy COO->CSR, a stable counting sort of row ids by bucket).
+// scipy COO->CSR, a stable counting sort of row ids by bucket).  With shift > 0
+// the rows are stably sorted by bucket group (h >> shift) instead -- the row
+// order the grouped apply kernels sweep -- and blo[] holds each row's bucket
+// inside its group.
 //
 // GPU form: a stable LSD radix sort of (key = h[i], value = i | sign<<31) with
 // 8-bit digits (ceil(log2 t / 8) passes), then indptr[b] = lower_bound(keys, b).
@@ -100,15 +103,16 @@ __global__ void identity_vals_kernel(const int8_t *__restrict__ sgn, int64_t n,
     rows[i] = (uint32_t)i | (sgn && sgn[i] < 0 ? 0x80000000u : 0u);
 }
 
-// indptr[b] = first position with key >= b, b in [0, t]
-__global__ void indptr_kernel(const uint32_t *__restrict__ keys, int64_t n, uint64_t t,
-                              int64_t *__restrict__ indptr) {
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= t;
+// indptr[g] = first position whose group (key >> shift) is >= g, g in [0, ngroups];
+// blo[i] = key & (2^shift - 1): the bucket inside its group.
+__global__ void indptr_kernel(const uint32_t *__restrict__ keys, int64_t n, uint64_t ngroups,
+                              int shift, int64_t *__restrict__ indptr) {
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= ngroups;
        b += (uint64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = n;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if ((uint64_t)keys[mid] < b)
+      if ((uint64_t)(keys[mid] >> shift) < b)
         lo = mid + 1;
       else
         hi = mid;
@@ -117,10 +121,17 @@ __global__ void indptr_kernel(const uint32_t *__restrict__ keys, int64_t n, uint
   }
 }
 
-int num_passes(uint64_t t) {
+__global__ void blo_kernel(const uint32_t *__restrict__ keys, int64_t n, uint32_t mask,
+                           uint8_t *__restrict__ blo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    blo[i] = (uint8_t)(keys[i] & mask);
+}
+
+int num_passes(uint64_t t, int shift) {
   if (t <= 1) return 0;
-  int bits = 64 - __builtin_clzll(t - 1);
-  return (bits + kBits - 1) / kBits;
+  const int bits = 64 - __builtin_clzll(t - 1) - shift;
+  return bits <= 0 ? 0 : (bits + kBits - 1) / kBits;
 }
 
 struct PlanWs {
@@ -128,7 +139,7 @@ struct PlanWs {
   size_t bytes;
 };
 
-PlanWs carve(void *ws, int64_t n, uint64_t t) {
+PlanWs carve(void *ws, int64_t n, uint64_t t, int shift) {
   PlanWs p{};
   const int64_t n_tiles = (n + kTile - 1) / kTile;
   const int64_t hist_len = (int64_t)kBins * n_tiles;
@@ -140,7 +151,7 @@ PlanWs carve(void *ws, int64_t n, uint64_t t) {
     off += align(bytes);
     return (uint32_t *)ptr;
   };
-  if (num_passes(t) > 0) {
+  if (num_passes(t, shift) > 0) {
     p.keys_a = take(sizeof(uint32_t) * n);
     p.keys_b = take(sizeof(uint32_t) * n);
     p.vals_b = take(sizeof(uint32_t) * n);
@@ -156,23 +167,26 @@ PlanWs carve(void *ws, int64_t n, uint64_t t) {
 
 using namespace skt;
 
-extern "C" skt_status skt_plan_workspace(int64_t n, uint64_t t, size_t *bytes) {
-  if (!bytes || n < 0 || n >= (1LL << 31) || t < 1 || t > (1ull << 32))
-    return fail(SKT_EINVAL, "skt_plan_workspace", "bad arguments (0 <= n < 2^31, 1 <= t <= 2^32)");
-  *bytes = carve(nullptr, n, t).bytes;
+extern "C" skt_status skt_plan_workspace(int64_t n, uint64_t t, int32_t shift, size_t *bytes) {
+  if (!bytes || n < 0 || n >= (1LL << 31) || t < 1 || t > (1ull << 32) || shift < 0 || shift > 8)
+    return fail(SKT_EINVAL, "skt_plan_workspace",
+                "bad arguments (0 <= n < 2^31, 1 <= t <= 2^32, 0 <= shift <= 8)");
+  *bytes = carve(nullptr, n, t, shift).bytes;
   return SKT_OK;
 }
 
 extern "C" skt_status skt_plan_build(const uint32_t *h, const int8_t *s, int64_t n, uint64_t t,
-                                     int64_t *indptr, uint32_t *rows, void *ws, size_t ws_bytes,
-                                     void *stream_) {
+                                     int32_t shift, int64_t *indptr, uint32_t *rows, uint8_t *blo,
+                                     void *ws, size_t ws_bytes, void *stream_) {
   static const char *fn = "skt_plan_build";
-  if (n < 0 || n >= (1LL << 31) || t < 1 || t > (1ull << 32) || !indptr || (n > 0 && (!h || !rows)))
-    return fail(SKT_EINVAL, fn, "bad arguments (0 <= n < 2^31, 1 <= t <= 2^32)");
+  if (n < 0 || n >= (1LL << 31) || t < 1 || t > (1ull << 32) || shift < 0 || shift > 8 || !indptr ||
+      (n > 0 && (!h || !rows)) || (shift > 0 && n > 0 && !blo))
+    return fail(SKT_EINVAL, fn, "bad arguments (0 <= n < 2^31, 1 <= t <= 2^32, 0 <= shift <= 8)");
   cudaStream_t stream = as_stream(stream_);
-  const PlanWs p = carve(ws, n, t);
+  const PlanWs p = carve(ws, n, t, shift);
   if (p.bytes > 0 && (!ws || ws_bytes < p.bytes)) return fail(SKT_EWORKSPACE, fn, "workspace too small");
-  const int passes = num_passes(t);
+  const int passes = num_passes(t, shift);
+  const uint64_t ngroups = ((t - 1) >> shift) + 1;
   const uint32_t *sorted_keys = h;
   if (n > 0 && passes == 0) {
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
@@ -185,26 +199,30 @@ extern "C" skt_status skt_plan_build(const uint32_t *h, const int8_t *s, int64_t
     for (int pass = 0; pass < passes; ++pass) {
       uint32_t *kout = (pass & 1) ? p.keys_b : p.keys_a;
       uint32_t *vout = ((passes - 1 - pass) & 1) ? p.vals_b : rows;
-      const int shift = pass * kBits;
-      SKT_LAUNCH(upsweep_kernel, (unsigned)n_tiles, kThreads, 0, stream, kin, n, shift, n_tiles,
+      const int bit = shift + pass * kBits;
+      SKT_LAUNCH(upsweep_kernel, (unsigned)n_tiles, kThreads, 0, stream, kin, n, bit, n_tiles,
                  p.tile_hist);
       skt_status st = exclusive_scan_u32(p.tile_hist, hist_len, p.partials, stream, fn);
       if (st != SKT_OK) return st;
       if (pass == 0)
         SKT_LAUNCH(downsweep_kernel<true>, (unsigned)n_tiles, kThreads, 0, stream, kin, nullptr, s,
-                   kout, vout, n, shift, n_tiles, p.tile_hist);
+                   kout, vout, n, bit, n_tiles, p.tile_hist);
       else
         SKT_LAUNCH(downsweep_kernel<false>, (unsigned)n_tiles, kThreads, 0, stream, kin, vin,
-                   nullptr, kout, vout, n, shift, n_tiles, p.tile_hist);
+                   nullptr, kout, vout, n, bit, n_tiles, p.tile_hist);
       kin = kout;
       vin = vout;
     }
     sorted_keys = kin;
   }
   {
-    const uint64_t work = t + 1;
+    const uint64_t work = ngroups + 1;
     const uint64_t blocks = std::min<uint64_t>((work + 255) / 256, 148ull * 16);
-    SKT_LAUNCH(indptr_kernel, (unsigned)blocks, 256, 0, stream, sorted_keys, n, t, indptr);
+    SKT_LAUNCH(indptr_kernel, (unsigned)blocks, 256, 0, stream, sorted_keys, n, ngroups, shift, indptr);
+  }
+  if (shift > 0 && n > 0) {
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    SKT_LAUNCH(blo_kernel, (unsigned)blocks, 256, 0, stream, sorted_keys, n, (1u << shift) - 1u, blo);
   }
   return check_launch(fn);
 }

@@ -231,18 +231,52 @@ class SparseEmbedding(SketchOperator):
                     _ptr(ws), nb.value, stream,
                 )
             )
-            self.plan_indptr = torch.empty(t + 1, dtype=torch.int64, device=dev)
-            self.plan_rows = torch.empty(m, dtype=torch.int32, device=dev)
-            check(L.skt_plan_workspace(m, t, ctypes.byref(nb)))
-            ws2 = _workspace(nb.value, dev)
-            check(
-                L.skt_plan_build(
-                    _ptr(self.h), _ptr(self.s), m, t, _ptr(self.plan_indptr), _ptr(self.plan_rows),
-                    _ptr(ws2), nb.value, stream,
-                )
-            )
+            self.plan_indptr, self.plan_rows, _, ws2 = self._build_plan(0, stream)
             # keep the workspaces alive until the stream has consumed them
             self._build_ws = (ws, ws2)
+            self._grouped = {0: (self.plan_indptr, self.plan_rows, None)}
+
+    def _build_plan(self, shift: int, stream):
+        """K2: rows stably sorted by bucket (shift 0) or bucket group h >> shift."""
+        L = _lib.lib()
+        dev, t = self.device, self.output_dim
+        m = self.row_end - self.row_begin
+        ngroups = ((t - 1) >> shift) + 1
+        indptr = torch.empty(ngroups + 1, dtype=torch.int64, device=dev)
+        rows = torch.empty(m, dtype=torch.int32, device=dev)
+        blo = torch.empty(m, dtype=torch.uint8, device=dev) if shift > 0 else None
+        nb = ctypes.c_size_t()
+        check(L.skt_plan_workspace(m, t, shift, ctypes.byref(nb)))
+        ws = _workspace(nb.value, dev)
+        check(
+            L.skt_plan_build(
+                _ptr(self.h), _ptr(self.s), m, t, shift, _ptr(indptr), _ptr(rows), _ptr(blo),
+                _ptr(ws), nb.value, stream,
+            )
+        )
+        return indptr, rows, blo, ws
+
+    def grouped_plan(self, shift: int):
+        """Plan with rows sorted by bucket group h >> shift (cached per shift)."""
+        if shift not in self._grouped:
+            with torch.cuda.device(self.device):
+                indptr, rows, blo, ws = self._build_plan(shift, _stream_ptr(self.device))
+                self._grouped[shift] = (indptr, rows, blo)
+                self._grouped_ws = ws
+        return self._grouped[shift]
+
+    def csr_group_shift(self, d: int, canonical: bool, nnz: int | None = None) -> int:
+        """Plan granularity for the CSR kernels.  Short canonical rows (mean
+        <= 8 nonzeros) use the grouped sweep: 2^shift buckets per warp, about
+        one warp per group across the chip (148 SMs x 32 warps), group
+        accumulators <= 24 KB.  Everything else sweeps the per-bucket plan."""
+        m = self.row_end - self.row_begin
+        if not canonical or nnz is None or m == 0 or nnz > 8 * m:
+            return 0
+        shift, resident = 0, 148 * 32
+        while shift < 8 and (self.output_dim >> shift) > resident and (2 << shift) * d * 8 <= 24 * 1024:
+            shift += 1
+        return shift
 
     # ---- host views (lazy; for API / test compatibility) -------------------
     @property
@@ -352,18 +386,22 @@ class SparseEmbedding(SketchOperator):
             raise ValueError("matrix contains non-finite entries")
         return out
 
-    def _apply_csr_device(self, indptr, indices, vals, d: int, out_dtype, canonical: bool, out=None):
+    def _apply_csr_device(self, indptr, indices, vals, d: int, out_dtype, canonical: bool, out=None,
+                          shift=None):
         if vals.dtype not in _TORCH_TO_SKT:
             vals = vals.to(torch.float64)
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
+        if shift is None:
+            shift = self.csr_group_shift(d, canonical, vals.numel())
+        gptr, grows, gblo = self.grouped_plan(shift)
         with torch.cuda.device(self.device):
             check(
                 _lib.lib().skt_apply_csr(
-                    _ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim,
+                    _ptr(gptr), _ptr(grows), _ptr(gblo), shift, self.output_dim,
                     self.row_end - self.row_begin, _ptr(indptr), _ITYPE[indptr.dtype], _ptr(indices),
-                    _ITYPE[indices.dtype], _ptr(vals), _TORCH_TO_SKT[vals.dtype], d, _ptr(out),
-                    _TORCH_TO_SKT[out.dtype], max(d, 1),
+                    _ITYPE[indices.dtype], _ptr(vals), _TORCH_TO_SKT[vals.dtype], vals.numel(), d,
+                    _ptr(out), _TORCH_TO_SKT[out.dtype], max(d, 1),
                     _lib.SKT_CSR_CANONICAL if canonical else 0, _stream_ptr(self.device),
                 )
             )

@@ -87,9 +87,11 @@ def test_device_entry_points_validate_before_touching_cuda():
     assert L.skt_hash_signs(ctypes.byref(st), ctypes.byref(st), 0, 10, 2**32 + 1, None, None, None, 0, None) == _lib.SKT_EINVAL
     assert "bad arguments" in _lib.last_error()
     nb = ctypes.c_size_t()
-    assert L.skt_plan_workspace(2**31, 10, ctypes.byref(nb)) == _lib.SKT_EINVAL
-    assert L.skt_plan_workspace(1000, 1 << 16, ctypes.byref(nb)) == 0 and nb.value > 0
-    assert L.skt_plan_workspace(1000, 1, ctypes.byref(nb)) == 0 and nb.value == 0
+    assert L.skt_plan_workspace(2**31, 10, 0, ctypes.byref(nb)) == _lib.SKT_EINVAL
+    assert L.skt_plan_workspace(1000, 10, 9, ctypes.byref(nb)) == _lib.SKT_EINVAL
+    assert L.skt_plan_workspace(1000, 1 << 16, 0, ctypes.byref(nb)) == 0 and nb.value > 0
+    assert L.skt_plan_workspace(1000, 1, 0, ctypes.byref(nb)) == 0 and nb.value == 0
+    assert L.skt_plan_workspace(1000, 256, 8, ctypes.byref(nb)) == 0 and nb.value == 0
     # lda < d
     assert L.skt_apply_dense(None, None, 4, 10, None, 0, 8, 4, None, 1, 8, None, None) == _lib.SKT_EINVAL
     with pytest.raises(ValueError):

@@ -89,6 +89,49 @@ def test_plan_matches_stable_counting_sort(n, t):
     assert np.array_equal((got_rows >> 31).astype(bool), s[rows] < 0)
 
 
+@pytest.mark.parametrize("n,t,shift", [(1000, 7, 1), (100_000, 4000, 3), (300_000, 16_384, 2), (50_000, 300, 8),
+                                       (20_000, 257, 4), (5000, 1, 2), (4_194_304, 16_384, 2)])
+def test_grouped_plan_is_stable_sort_by_group(n, t, shift):
+    op = SparseEmbedding(n, t, seed=3)
+    h, s = O.hash_signs(n, t, 3)
+    gptr, grows, gblo = op.grouped_plan(shift)
+    order = np.argsort(h >> shift, kind="stable")
+    got = grows.cpu().numpy().view(np.uint32)
+    assert np.array_equal((got & 0x7FFFFFFF).astype(np.int64), order)
+    assert np.array_equal((got >> 31).astype(bool), s[order] < 0)
+    assert np.array_equal(gblo.cpu().numpy(), (h[order] & ((1 << shift) - 1)).astype(np.uint8))
+    ngroups = ((t - 1) >> shift) + 1
+    want = np.searchsorted(h[order] >> shift, np.arange(ngroups + 1), side="left")
+    assert np.array_equal(gptr.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("t,d", [(1000, 48), (37, 5), (33, 700), (4096, 1)])
+def test_apply_csr_bucket_lane_kernel(dtype, t, d, rng):
+    """Long rows (> 16 nonzeros), empty rows, partial last warp of buckets."""
+    n = 20_000
+    shift = 0
+    a = sp.csr_array(sp.random_array((n, d), density=0.15, rng=rng, format="csr"), dtype=dtype)
+    # a few long rows (> 16 nonzeros) and empty rows
+    a = a.tolil()
+    a[17, :] = rng.standard_normal(d)
+    a[18, :] = 0
+    a[19000, ::2] = rng.standard_normal(len(range(0, d, 2)))
+    a = sp.csr_array(a, dtype=dtype)
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    ref = O.np_apply_csr(h, s, t, a)
+    dev = [torch.from_numpy(x).cuda() for x in (a.indptr, a.indices, a.data)]
+    got = op._apply_csr_device(*dev, d, torch.float64, canonical=True, shift=shift)
+    assert np.array_equal(got.cpu().numpy(), ref)
+    for gshift in (1, 3):  # grouped sweep kernel over bucket-group plans
+        if (1 << gshift) * d * 8 <= 24 * 1024:
+            got = op._apply_csr_device(*dev, d, torch.float64, canonical=True, shift=gshift)
+            assert np.array_equal(got.cpu().numpy(), ref), gshift
+    with pytest.raises(ValueError):  # non-canonical input needs the per-bucket plan
+        op._apply_csr_device(*dev, d, torch.float64, canonical=False, shift=2)
+
+
 def test_host_views_match_reference_layout():
     op = make_sparse_embedding(9, 5, seed=1)
     h, s = O.hash_signs(9, 5, 1)
