@@ -15,7 +15,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsketch_b200.so")
+LIB_PATH = os.environ.get("SKT_LIB_PATH") or os.path.join(_HERE, "libsketch_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 SKT_OK, SKT_EINVAL, SKT_ECUDA, SKT_ENOTSUP, SKT_EWORKSPACE = range(5)

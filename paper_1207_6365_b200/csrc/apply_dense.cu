@@ -10,12 +10,18 @@
 // result is bit-identical.  Rows are gathered with 128-bit non-allocating
 // loads, kUnroll rows in flight per lane before the ordered accumulation.
 // The non-finite check of as_dense is fused (exponent-all-ones test).
+#include <cstdlib>
+
 #include "common.cuh"
+#include "dense_tma.cuh"
 
 namespace skt {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef SKT_DENSE_MINB
+#define SKT_DENSE_MINB 4
+#endif
 
 template <typename T, int VEC>
 struct Vec;
@@ -78,7 +84,7 @@ __device__ __forceinline__ bool nonfinite(double x) {
 }
 
 template <typename TIn, typename TOut, int VEC, int G, int kUnroll>
-__global__ void __launch_bounds__(kThreads) apply_dense_kernel(
+__global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
     const int64_t *__restrict__ indptr, const uint32_t *__restrict__ rows, int64_t n_items,
     int64_t n_chunks, const TIn *__restrict__ a, int64_t d, int64_t lda, TOut *__restrict__ sa,
     int64_t ldsa, int32_t *__restrict__ flag) {
@@ -102,17 +108,27 @@ __global__ void __launch_bounds__(kThreads) apply_dense_kernel(
   const int64_t beg = live ? indptr[bucket] : 0;
   const int64_t end = live ? indptr[bucket + 1] : 0;
   const TIn *acol = a + col;
+  // plan words of the next kUnroll rows are loaded one iteration ahead, so
+  // each iteration waits for one DRAM round trip (the row gather) only
+  uint32_t wn[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) wn[u] = (beg + u < end) ? __ldg(rows + beg + u) : 0u;
   for (int64_t k0 = beg; k0 < end; k0 += kUnroll) {
     uint32_t w[kUnroll];
     V v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) w[u] = (k0 + u < end) ? __ldg(rows + k0 + u) : 0u;
+    for (int u = 0; u < kUnroll; ++u) w[u] = wn[u];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (active && k0 + u < end)
         v[u] = ldstream(reinterpret_cast<const V *>(acol + (int64_t)(w[u] & 0x7fffffffu) * lda));
       else
         v[u] = V{};
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t k = k0 + kUnroll + u;
+      wn[u] = (k < end) ? __ldg(rows + k) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -148,7 +164,7 @@ skt_status launch(const int64_t *indptr, const uint32_t *rows, uint64_t t, const
   const int64_t n_items = (int64_t)t * n_chunks;
   const int64_t warps = (n_items + (32 / G) - 1) / (32 / G);
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  constexpr int kUnroll = (sizeof(TIn) * VEC >= 16) ? 8 : 16;
+  constexpr int kUnroll = (sizeof(TIn) * VEC >= 16) ? 4 : 8;
   SKT_LAUNCH((apply_dense_kernel<TIn, TOut, VEC, G, kUnroll>), (unsigned)blocks, kThreads, 0, stream,
              indptr, rows, n_items, n_chunks, a, d, lda, sa, ldsa, flag);
   return check_launch("skt_apply_dense");
@@ -167,6 +183,15 @@ skt_status dispatch_g(const int64_t *indptr, const uint32_t *rows, uint64_t t, c
   return launch<TIn, TOut, VEC, 32>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
 }
 
+// SKT_DENSE_TMA=0 selects the register-gather kernel (A/B measurement).
+inline bool tma_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_DENSE_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename TIn, typename TOut>
 skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a_,
                         int64_t d, int64_t lda, void *sa_, int64_t ldsa, int32_t *flag,
@@ -177,6 +202,22 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
   auto ok = [&](int vec) {
     return d % vec == 0 && lda % vec == 0 && ap % (sizeof(TIn) * vec) == 0;
   };
+  // bulk-copy (TMA 1D) gather for rows of 1-2 KB (16-byte multiples).  Shorter
+  // rows stay on the register gather: a 1D bulk copy costs ~46 SM cycles of TMA
+  // issue, which caps 512 B rows at ~3.8 TB/s (measured, profiles/).
+  const int64_t row_bytes = d * (int64_t)sizeof(TIn), lda_bytes = lda * (int64_t)sizeof(TIn);
+  if (tma_enabled() && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 1024 &&
+      row_bytes <= 2048) {
+    const int kchunks = (int)((row_bytes + 511) / 512);
+    const size_t smem = dense_tma_smem((int)row_bytes);
+    const int64_t blocks = ((int64_t)t + kTmaWarps - 1) / kTmaWarps;
+    auto k = kchunks <= 1 ? dense_tma_kernel<TIn, TOut, 1>
+                          : kchunks <= 2 ? dense_tma_kernel<TIn, TOut, 2> : dense_tma_kernel<TIn, TOut, 4>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_dense");
+    SKT_LAUNCH(k, (unsigned)blocks, kTmaWarps * 32, smem, stream, indptr, rows, t, (const char *)a,
+               (int)row_bytes, lda_bytes, (int)d, sa, ldsa, flag);
+    return check_launch("skt_apply_dense");
+  }
   if (sizeof(TIn) == 4 && ok(4))
     return dispatch_g<TIn, TOut, (sizeof(TIn) == 4 ? 4 : 2)>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
   if (ok(2)) return dispatch_g<TIn, TOut, 2>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);

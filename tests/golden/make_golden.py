@@ -146,7 +146,7 @@ def configs():
     sol = sketch_solve_ls(a, b, eps=0.5, seed=seed, operator=op)
     res["config1"] = {
         "n": a.shape[0], "d": a.shape[1], "t": 4000, "seed": seed,
-        "sha_a": sha(a), "sha_h": sha(op.bucket.astype(np.uint32)), "sha_s": sha(op.sign.astype(np.int8)),
+        "sha_a": sha(a), "sha_b": sha(b), "sha_h": sha(op.bucket.astype(np.uint32)), "sha_s": sha(op.sign.astype(np.int8)),
         "sha_sa": sha(sa), "sha_sb": sha(sb), "sha_x": sha(sol.x),
         "x": sol.x.ravel().tolist(), "residual_norm": sol.residual_norm,
         "sa_fro": float(np.linalg.norm(sa)),
@@ -159,7 +159,7 @@ def configs():
     sol = sketch_solve_ls(a, b, eps=0.5, seed=seed, operator=op)
     res["config2"] = {
         "n": a.shape[0], "d": a.shape[1], "t": 25000, "seed": seed,
-        "sha_indices": sha(a.indices), "sha_data": sha(a.data),
+        "sha_indices": sha(a.indices), "sha_data": sha(a.data), "sha_b": sha(b),
         "sha_h": sha(op.bucket.astype(np.uint32)), "sha_s": sha(op.sign.astype(np.int8)),
         "sha_sa": sha(sa), "sha_sb": sha(sb), "sha_x": sha(sol.x),
         "x": sol.x.ravel().tolist(), "residual_norm": sol.residual_norm,

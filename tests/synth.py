@@ -29,12 +29,21 @@ def csr_fixed_nnz(rng, n: int, d: int, per_row: int, dtype=np.float64, scale: fl
     return sp.csr_array((vals, cols.ravel(), indptr), shape=(n, d))
 
 
+def matvec_fixed_order(a: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """A @ x with a fixed summation order (elementwise ufuncs, no BLAS), so the
+    generated right-hand side is bit-identical on every host CPU."""
+    acc = a[:, 0] * x[0, 0]
+    for j in range(1, a.shape[1]):
+        acc = acc + a[:, j] * x[j, 0]
+    return acc.reshape(-1, 1)
+
+
 def config1():
     """C1: dense fp64 100,000 x 20 ~ N(0,1); b = A x* + 0.1 N(0,1); m = 4,000."""
     rng = np.random.default_rng(101)
     a = rng.standard_normal((100_000, 20))
     x = rng.standard_normal((20, 1))
-    b = a @ x + 0.1 * rng.standard_normal((100_000, 1))
+    b = matvec_fixed_order(a, x) + 0.1 * rng.standard_normal((100_000, 1))
     return a, b, SKETCH_SEED
 
 

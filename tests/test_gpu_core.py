@@ -326,5 +326,6 @@ def test_leverage_pipeline_matches_reference_pieces():
     run = leverage_scores_sketched(a, m, k, seed)
     assert sha(run.sa) == cfg["sha_sa"]  # GPU S.A bit-identical to the reference
     assert run.rank == cfg["rank"]
-    assert sha(run.probe) == cfg["sha_probe"]
+    # the probe comes from the host QR / inverse (LAPACK: last bits host-dependent)
+    assert np.linalg.norm(run.probe - z["probe"]) <= 1e-12 * np.linalg.norm(z["probe"])
     assert np.max(np.abs(run.scores - z["scores"]) / np.abs(z["scores"])) <= 1e-12
