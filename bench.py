@@ -289,8 +289,27 @@ def our_arm(args, cfg):
     SA = torch.empty((m, d), dtype=sa_dt, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    lev = None
+    if args.kernel == "lev":
+        # K5: leverage contraction rows = A @ (R^-1 G), squared row norms (config 4 pipeline)
+        from paper_1207_6365_b200.solvers import basis_change, gaussian_jl_entries
+
+        sa64 = op._apply_csr_device(ip, ix, vv, d, torch.float64, canonical=True).cpu().numpy()
+        n_mat, qr_rank = basis_change(sa64)
+        probe = torch.from_numpy(n_mat @ gaussian_jl_entries(32, qr_rank, 7).T).to(dev)
+        scores = torch.empty(nnz_local and (r1 - r0), dtype=torch.float64, device=dev)
+        lev = (probe, scores)
+
     def apply_once():
-        if cfg["kind"] == "dense":
+        if lev is not None:
+            from paper_1207_6365_b200 import _lib
+            from paper_1207_6365_b200.sketch import _ITYPE, _TORCH_TO_SKT, _ptr, _stream_ptr
+
+            _lib.check(_lib.lib().skt_lev_rownorms_csr(
+                r1 - r0, d, _ptr(ip), _ITYPE[ip.dtype], _ptr(ix), _ITYPE[ix.dtype], _ptr(vv),
+                _TORCH_TO_SKT[vv.dtype], _ptr(lev[0]), lev[0].shape[1], _ptr(lev[1]), _lib.SKT_F64,
+                _stream_ptr(dev)))
+        elif cfg["kind"] == "dense":
             op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
         else:
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA)
@@ -301,7 +320,7 @@ def our_arm(args, cfg):
         apply_once()
         if kev is not None:
             kev[1].record(stream)
-        if world > 1:
+        if world > 1 and lev is None:
             dist.all_reduce(SA)
 
     for _ in range(args.warmup):
@@ -350,7 +369,7 @@ def our_arm(args, cfg):
     value = nnz_total / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (this rank's apply launch)
-    alg_bytes = in_bytes + m * d * SA.element_size()
+    alg_bytes = in_bytes + (m * d * SA.element_size() if lev is None else (r1 - r0) * 8)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -418,6 +437,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--kernel", default="sa", choices=["sa", "lev"],
+                    help="sa: the S.A hot path (headline); lev: K5 leverage contraction (config c4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

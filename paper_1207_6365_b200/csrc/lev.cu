@@ -10,7 +10,24 @@
 // next row's nonzeros are prefetched while the current row is contracted.
 // Per (row, column) the products are accumulated in stored-nonzero order with
 // fp64 FMA; the 32-lane square-sum uses a fixed butterfly (deterministic).
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
+#include "lev_tc.cuh"
+
+namespace skt {
+namespace {
+// SKT_LEV_TC=0 keeps fp32 inputs on the fp64 CUDA-core path (A/B checks).
+inline bool lev_tc_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_LEV_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace
+}  // namespace skt
 
 namespace skt {
 namespace {
@@ -116,6 +133,21 @@ template <typename IP, typename IX, typename TV, typename TS>
 skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, const void *av,
                       const double *p, int64_t k, void *scores, cudaStream_t st) {
   static const char *fn = "skt_lev_rownorms_csr";
+  // fp32 values on the tensor cores (3xTF32, tcgen05) when the shape fits
+  if (std::is_same<TV, float>::value && lev_tc_enabled() && d <= 256 && k >= 8 && k <= 256 && k % 8 == 0) {
+    const int dk = (int)((d + 7) & ~7LL);
+    const size_t smem = lev_tc_smem(dk, (int)k);
+    if (smem <= 200 * 1024) {
+      auto kern = lev_tc_kernel<IP, IX, TS>;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+      const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / smem));
+      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm);
+      SKT_LAUNCH(kern, (unsigned)blocks, kTcThreads, smem, st, n, (int)d, dk, (const IP *)aip,
+                 (const IX *)aix, (const float *)av, p, (int)k, (TS *)scores);
+      return check_launch(fn);
+    }
+  }
   const size_t pbytes = (size_t)d * k * sizeof(double);
   const int64_t blocks = grid_for(n);
   if (pbytes <= kProbeSmemMax) {

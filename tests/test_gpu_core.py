@@ -316,6 +316,24 @@ def test_lev_rownorms_golden():
     assert np.max(np.abs(gd - z["scores"]) / np.abs(z["scores"])) <= 1e-12
 
 
+@pytest.mark.parametrize("n,d,k,density", [(20_000, 64, 32, 0.26), (5_000, 16, 8, 0.5), (3_001, 100, 40, 0.1),
+                                           (4_000, 256, 256, 0.05), (1_000, 8, 16, 1.0)])
+def test_lev_tensor_core_3xtf32(n, d, k, density, rng):
+    """fp32 CSR runs on tcgen05 (3xTF32): scores within 1e-5 of the fp64 oracle."""
+    from paper_1207_6365_b200.solvers import lev_rownorms
+
+    a = sp.csr_array(sp.random_array((n, d), density=density, rng=rng, format="csr"), dtype=np.float32)
+    a = a.tolil()
+    a[5, :] = rng.standard_normal(d).astype(np.float32) * 10  # a dense row (long-row path)
+    a = sp.csr_array(a, dtype=np.float32)
+    probe = rng.standard_normal((d, k)) / np.sqrt(k)
+    ref = O.lev_rownorms_csr(a, probe)
+    got = lev_rownorms(a, probe)
+    nz = ref > 0
+    assert np.all(got[~nz] == 0)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-5
+
+
 def test_leverage_pipeline_matches_reference_pieces():
     from paper_1207_6365_b200.solvers import leverage_scores_sketched
     from tests import synth
