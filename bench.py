@@ -40,6 +40,10 @@ CONFIGS = {
                workload="config3: dense fp32 16777216x128 (rows N(0,1)*lognormal(0,1)), m=65536, S.A row-sharded + all-reduce"),
     "c4": dict(kind="csr", n=4_194_304, d=64, m=16_384, dtype="f32", per_row=16, dense_frac=0.01, seed=1,
                workload="config4: CSR fp32 4194304x64, 16 nnz/row + 1% dense rows N(0,100), m=16384"),
+    "c5": dict(kind="csr", n=262_144, d=262_144, m=400, dtype="f32", per_row=262, lowrank=10, seed=1,
+               fast=True,
+               workload="config5: CSR fp32 262144x262144, 262 nnz/row (0.1%), values (U V^T)_ij + 0.01 N, "
+                        "rank 10; m=400 row sketch (fast mode: unordered fp32 atomics)"),
 }
 
 
@@ -145,9 +149,42 @@ def gen_dense_shard(torch, cfg, r0, r1, device):
     return out
 
 
+def gen_lowrank_csr_shard(torch, cfg, r0, r1, device):
+    """Config 5: rows [r0, r1) of a square CSR with `per_row` distinct columns
+    per row (one uniform column in each of `per_row` equal column strata, so
+    they are distinct and sorted), values (U V^T)_ij + 0.01 N(0,1) with
+    U, V ~ N(0,1)^{n x k}; generated in row chunks with per-chunk seeds."""
+    n, d, per, k = cfg["n"], cfg["d"], cfg["per_row"], cfg["lowrank"]
+    dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(99)
+    V = torch.randn((d, k), generator=g, device=device)
+    stride = d // per
+    m = r1 - r0
+    indices = torch.empty(m * per, dtype=torch.int32, device=device)
+    vals = torch.empty(m * per, dtype=dt, device=device)
+    chunk = 1 << 14
+    for c0 in range(r0 - r0 % chunk, r1, chunk):
+        c1 = min(c0 + chunk, n)
+        g.manual_seed(5_000_011 + c0 // chunk)
+        U = torch.randn((c1 - c0, k), generator=g, device=device)
+        cols = (torch.arange(per, device=device) * stride)[None, :] + torch.randint(
+            0, stride, (c1 - c0, per), generator=g, device=device)
+        v = (U[:, None, :] * V[cols]).sum(-1) + 0.01 * torch.randn((c1 - c0, per), generator=g, device=device)
+        lo, hi = max(c0, r0), min(c1, r1)
+        indices[(lo - r0) * per:(hi - r0) * per] = cols[lo - c0:hi - c0].reshape(-1).to(torch.int32)
+        vals[(lo - r0) * per:(hi - r0) * per] = v[lo - c0:hi - c0].reshape(-1).to(dt)
+    indptr = torch.arange(0, (m + 1) * per, per, device=device, dtype=torch.int64)
+    if m * per < 2**31:
+        indptr = indptr.to(torch.int32)
+    return indptr, indices, vals
+
+
 def gen_csr_shard(torch, cfg, r0, r1, device):
     """CSR rows [r0, r1): `per_row` distinct uniform columns per row, N(0,1)
     values; a `dense_frac` of rows fully dense with N(0, 100) values (c4)."""
+    if cfg.get("lowrank"):
+        return gen_lowrank_csr_shard(torch, cfg, r0, r1, device)
     d, per = cfg["d"], cfg["per_row"]
     dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
     g = torch.Generator(device=device)
@@ -312,7 +349,8 @@ def our_arm(args, cfg):
         elif cfg["kind"] == "dense":
             op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
         else:
-            op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA)
+            op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
+                                 deterministic=not cfg.get("fast", False))
 
     def step(kev=None):
         if kev is not None:

@@ -39,6 +39,7 @@ typedef enum skt_itype { SKT_I32 = 0, SKT_I64 = 1 } skt_itype;
 
 /* flags for skt_apply_csr */
 #define SKT_CSR_CANONICAL 1u /* no duplicate column inside a row (as_csr output) */
+#define SKT_CSR_FAST 2u      /* allow unordered global atomics: not deterministic, SA to rounding */
 
 /* 128-bit PCG64 state (numpy's PCG64: state and odd increment), hi/lo words. */
 typedef struct skt_pcg64 {

@@ -22,6 +22,7 @@ SKT_OK, SKT_EINVAL, SKT_ECUDA, SKT_ENOTSUP, SKT_EWORKSPACE = range(5)
 SKT_F32, SKT_F64 = 0, 1
 SKT_I32, SKT_I64 = 0, 1
 SKT_CSR_CANONICAL = 1
+SKT_CSR_FAST = 2
 
 # Every symbol include/sketch_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (

@@ -12,12 +12,14 @@
 // therefore happen in ascending row order, exactly as the bincount does --
 // bit-identical fp64.  Non-canonical rows (duplicate columns) are serialised
 // in stored order with __match_any_sync.
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
 #include "csr_group.cuh"
 #include "csr_lane.cuh"
 #include "csr_tile.cuh"
+#include "csr_wide.cuh"
 
 namespace skt {
 namespace {
@@ -131,8 +133,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32) apply_csr_kernel(
 template <typename IP, typename IX, typename TV, typename TOut>
 skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
                   uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
-                  int64_t nnz, int64_t d, void *sa, int64_t ldsa, bool canon, cudaStream_t stream) {
+                  int64_t nnz, int64_t d, void *sa, int64_t ldsa, uint32_t flags, cudaStream_t stream) {
   static const char *fn = "skt_apply_csr";
+  const bool canon = (flags & SKT_CSR_CANONICAL) != 0;
+  if (flags & SKT_CSR_FAST) {  // unordered atomics into a zeroed SA (any d)
+    if (shift != 0) return fail(SKT_EINVAL, fn, "fast mode needs the per-bucket plan (shift 0)");
+    SKT_CUDA_TRY(cudaMemset2DAsync(sa, ldsa * sizeof(TOut), 0, d * sizeof(TOut), t, stream), fn);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)kNumSMs * 16));
+    SKT_LAUNCH((csr_atomic_kernel<IP, IX, TV, TOut>), (unsigned)blocks, 256, 0, stream, pindptr, prow, t, n,
+               (const IP *)aip, (const IX *)aix, (const TV *)av, (TOut *)sa, ldsa);
+    return check_launch(fn);
+  }
   const int64_t gb = 1LL << shift;
   const bool short_rows = n > 0 && nnz <= 8 * n;  // mean row length <= 8
   // (1) grouped sweep over a bucket-group plan (short rows)
@@ -176,7 +187,16 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
   const size_t per_warp = WarpSmem::bytes(d);
   const size_t kSmemMax = 200 * 1024;
   int warps = (int)std::min<size_t>(kMaxWarps, kSmemMax / per_warp);
-  if (warps < 1) return fail(SKT_ENOTSUP, fn, "d too wide for the shared-memory accumulator");
+  if (warps < 1) {
+    // (5) too wide for shared memory: warp per bucket, fp64 accumulation in the output row
+    if (!canon) return fail(SKT_ENOTSUP, fn, "non-canonical CSR this wide is not supported");
+    if (!std::is_same<TOut, double>::value)
+      return fail(SKT_ENOTSUP, fn, "deterministic wide-d CSR writes fp64 SA (round on the host side)");
+    const int64_t blocks = ((int64_t)t + 3) / 4;
+    SKT_LAUNCH((csr_rowseq_kernel<IP, IX, TV, TOut>), (unsigned)blocks, 128, 0, stream, pindptr, prow, t,
+               (const IP *)aip, (const IX *)aix, (const TV *)av, d, (double *)nullptr, (TOut *)sa, ldsa);
+    return check_launch(fn);
+  }
   const size_t smem = per_warp * warps;
   const int64_t blocks = ((int64_t)t + warps - 1) / warps;
   auto k = canon ? apply_csr_kernel<IP, IX, TV, TOut, true> : apply_csr_kernel<IP, IX, TV, TOut, false>;
@@ -190,12 +210,12 @@ template <typename IP, typename IX>
 skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
                    uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
                    skt_dtype vt, int64_t nnz, int64_t d, void *sa, skt_dtype ot, int64_t ldsa,
-                   bool canon, cudaStream_t s) {
+                   uint32_t flags, cudaStream_t s) {
   if (vt == SKT_F32)
-    return ot == SKT_F64 ? launch<IP, IX, float, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s)
-                         : launch<IP, IX, float, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s);
-  return ot == SKT_F64 ? launch<IP, IX, double, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s)
-                       : launch<IP, IX, double, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, canon, s);
+    return ot == SKT_F64 ? launch<IP, IX, float, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, flags, s)
+                         : launch<IP, IX, float, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, flags, s);
+  return ot == SKT_F64 ? launch<IP, IX, double, double>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, flags, s)
+                       : launch<IP, IX, double, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, flags, s);
 }
 
 }  // namespace
@@ -221,12 +241,11 @@ extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows,
   if (d == 0) return SKT_OK;
   if (!sa || (n > 0 && !rows)) return fail(SKT_EINVAL, fn, "NULL buffer");
   cudaStream_t s = as_stream(stream_);
-  const bool canon = (flags & SKT_CSR_CANONICAL) != 0;
   if (indptr_type == SKT_I32)
     return index_type == SKT_I32
-               ? by_vals<int32_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s)
-               : by_vals<int32_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s);
+               ? by_vals<int32_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s)
+               : by_vals<int32_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s);
   return index_type == SKT_I32
-             ? by_vals<int64_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s)
-             : by_vals<int64_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, canon, s);
+             ? by_vals<int64_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s)
+             : by_vals<int64_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s);
 }

@@ -313,11 +313,13 @@ class SparseEmbedding(SketchOperator):
         if nrows != want:
             raise ValueError(f"operator expects {want} rows, got {nrows}")
 
-    def apply(self, a, out_dtype=None, check_finite: bool = True):
+    def apply(self, a, out_dtype=None, check_finite: bool = True, deterministic: bool = True):
         """S @ a (sketch.py:153-165).  Returns float64 unless ``out_dtype``.
 
         numpy / scipy input -> new numpy array; torch input -> torch tensor on
         the input's device (CPU tensors are staged through the GPU).
+        ``deterministic=False`` lets sparse input use unordered atomics (equal
+        to the reference up to rounding, not bit-for-bit).
         """
         if self.row_begin == 0 and self.row_end == self.input_dim:
             self._check_rows(a)
@@ -326,12 +328,11 @@ class SparseEmbedding(SketchOperator):
         if isinstance(a, torch.Tensor):
             out_t = torch.float64 if out_dtype is None else out_dtype
             if a.layout == torch.sparse_csr:
-                res = self._apply_csr_device(
-                    a.crow_indices(), a.col_indices(), a.values(), a.shape[1], out_t, canonical=False
-                ) if a.is_cuda else self._apply_csr_device(
-                    *(x.to(self.device, non_blocking=True) for x in (a.crow_indices(), a.col_indices(), a.values())),
-                    a.shape[1], out_t, canonical=False,
-                )
+                parts = (a.crow_indices(), a.col_indices(), a.values())
+                if not a.is_cuda:
+                    parts = tuple(x.to(self.device, non_blocking=True) for x in parts)
+                res = self._apply_csr_device(*parts, a.shape[1], out_t, canonical=False,
+                                             deterministic=deterministic)
                 return res if a.is_cuda else res.cpu()
             if a.is_cuda:
                 return self._apply_dense_device(a, out_t, check_finite)
@@ -347,7 +348,8 @@ class SparseEmbedding(SketchOperator):
             ip = torch.from_numpy(np.ascontiguousarray(m.indptr)).to(dev)
             ix = torch.from_numpy(np.ascontiguousarray(m.indices)).to(dev)
             vv = torch.from_numpy(np.ascontiguousarray(m.data)).to(dev)
-            return self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical).cpu().numpy()
+            return self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical,
+                                          deterministic=deterministic).cpu().numpy()
         arr = np.asarray(a)
         if arr.dtype not in (np.float32, np.float64):
             arr = arr.astype(np.float64)
@@ -386,23 +388,30 @@ class SparseEmbedding(SketchOperator):
             raise ValueError("matrix contains non-finite entries")
         return out
 
+    # widest d the shared-memory CSR kernels accumulate on chip (fp64 per warp)
+    _CSR_SMEM_MAX_D = (200 * 1024 - 3328) // 8
+
     def _apply_csr_device(self, indptr, indices, vals, d: int, out_dtype, canonical: bool, out=None,
-                          shift=None):
+                          shift=None, deterministic: bool = True):
         if vals.dtype not in _TORCH_TO_SKT:
             vals = vals.to(torch.float64)
+        if (deterministic and out_dtype == torch.float32 and d > self._CSR_SMEM_MAX_D and canonical
+                and out is None):
+            # the wide deterministic kernel accumulates in the fp64 output row
+            return self._apply_csr_device(indptr, indices, vals, d, torch.float64, canonical).to(torch.float32)
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
         if shift is None:
-            shift = self.csr_group_shift(d, canonical, vals.numel())
+            shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
         gptr, grows, gblo = self.grouped_plan(shift)
+        flags = (_lib.SKT_CSR_CANONICAL if canonical else 0) | (0 if deterministic else _lib.SKT_CSR_FAST)
         with torch.cuda.device(self.device):
             check(
                 _lib.lib().skt_apply_csr(
                     _ptr(gptr), _ptr(grows), _ptr(gblo), shift, self.output_dim,
                     self.row_end - self.row_begin, _ptr(indptr), _ITYPE[indptr.dtype], _ptr(indices),
                     _ITYPE[indices.dtype], _ptr(vals), _TORCH_TO_SKT[vals.dtype], vals.numel(), d,
-                    _ptr(out), _TORCH_TO_SKT[out.dtype], max(d, 1),
-                    _lib.SKT_CSR_CANONICAL if canonical else 0, _stream_ptr(self.device),
+                    _ptr(out), _TORCH_TO_SKT[out.dtype], max(d, 1), flags, _stream_ptr(self.device),
                 )
             )
         return out

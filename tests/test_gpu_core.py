@@ -277,6 +277,28 @@ def test_monte_carlo_unbiased():
     assert 3.8 <= total / 2000 <= 4.2
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_apply_csr_wide_d(dtype, rng):
+    """Config-5 shape (d too wide for on-chip accumulators): the deterministic
+    wide kernel is bit-exact; fast mode (unordered atomics) is within rounding."""
+    n, d, t = 6000, 60_000, 23
+    a = sp.csr_array(sp.random_array((n, d), density=0.002, rng=rng, format="csr"), dtype=dtype)
+    op = SparseEmbedding(n, t, seed=5)
+    h, s = O.hash_signs(n, t, 5)
+    ref = O.np_apply_csr(h, s, t, a)
+    assert np.array_equal(op.apply(a), ref)
+    got32 = op.apply(a, out_dtype=torch.float32)
+    assert np.array_equal(got32, ref.astype(np.float32))
+    fast = op.apply(a, deterministic=False)
+    assert np.linalg.norm(fast - ref) <= 1e-12 * np.linalg.norm(ref)
+    fast32 = op.apply(a, out_dtype=torch.float32, deterministic=False)
+    assert np.linalg.norm(fast32 - ref) <= 1e-5 * np.linalg.norm(ref)
+    # fast mode on a narrow matrix too
+    b = sp.csr_array(sp.random_array((n, 40), density=0.2, rng=rng, format="csr"), dtype=dtype)
+    ref_b = O.np_apply_csr(h, s, t, b)
+    assert np.linalg.norm(op.apply(b, deterministic=False) - ref_b) <= 1e-12 * np.linalg.norm(ref_b)
+
+
 # ---------------------------------------------------------------- column sketch
 def test_apply_right_golden():
     z = load("apply_cases.npz")
