@@ -352,9 +352,25 @@ def our_arm(args, cfg):
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
                                  deterministic=not cfg.get("fast", False))
 
+    # N > 1, dense: pipelined exchange -- SA is computed in contiguous bucket
+    # ranges and each range is all-reduced (async, NCCL stream) while the next
+    # range is computed (distributed.ShardedSparseEmbedding.apply(chunks=K)).
+    pipelined = world > 1 and cfg["kind"] == "dense" and lev is None and args.chunks > 1
+    ranges = [(k * m // args.chunks, (k + 1) * m // args.chunks) for k in range(args.chunks)]
+
     def step(kev=None):
         if kev is not None:
             kev[0].record(stream)
+        if pipelined:
+            works = []
+            for b0, b1 in ranges:
+                op._apply_dense_device(A, sa_dt, check_finite=False, out=SA, buckets=(b0, b1))
+                works.append(dist.all_reduce(SA[b0:b1], async_op=True))
+            if kev is not None:
+                kev[1].record(stream)
+            for w in works:
+                w.wait()
+            return
         apply_once()
         if kev is not None:
             kev[1].record(stream)
@@ -458,7 +474,9 @@ def our_arm(args, cfg):
                    "sa_dtype": "f32" if sa_dt == torch.float32 else "f64",
                    "accumulate": "fp64, ascending row order (bit-identical to the reference)",
                    "l2": "inputs larger than L2 (no flush needed)",
-                   "parallelism": f"row-shard x{world}" + (" + NCCL all-reduce of m x d partials" if world > 1 else "")},
+                   "parallelism": f"row-shard x{world}" + (
+                       (f" + NCCL all-reduce of m x d partials, pipelined over {args.chunks} bucket ranges"
+                        if pipelined else " + NCCL all-reduce of m x d partials") if world > 1 else "")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "remeasured": remeasured,
         "build_ms": round(build_ms, 3), "kernel_ms_max_over_ranks": round(kern_ms_max, 4),
@@ -477,6 +495,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--kernel", default="sa", choices=["sa", "lev"],
                     help="sa: the S.A hot path (headline); lev: K5 leverage contraction (config c4)")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="N > 1: bucket ranges whose all-reduce overlaps the next range's compute")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

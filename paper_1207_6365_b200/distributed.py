@@ -44,18 +44,48 @@ class ShardedSparseEmbedding:
             partial_fn = self._gpu_partial
         self.partial_fn = partial_fn
 
-    def _gpu_partial(self, a_local, out_dtype):
-        return self.local.apply(a_local, out_dtype=out_dtype)
+    def _gpu_partial(self, a_local, out_dtype, buckets=None, out=None):
+        if buckets is None:
+            return self.local.apply(a_local, out_dtype=out_dtype)
+        if out is None:
+            out = torch.empty((self.output_dim, a_local.shape[1]), dtype=out_dtype, device=a_local.device)
+        self.local._apply_dense_device(a_local, out_dtype, check_finite=False, out=out, buckets=buckets)
+        return out[buckets[0] : buckets[1]]
 
-    def apply(self, a_local, out_dtype=torch.float64, async_op: bool = False):
-        """Full S.A on every rank from this rank's rows ``a_local``."""
+    def bucket_chunks(self, chunks: int):
+        """Contiguous bucket ranges of the pipelined apply."""
+        t = self.output_dim
+        chunks = max(1, min(int(chunks), t))
+        return [(k * t // chunks, (k + 1) * t // chunks) for k in range(chunks)]
+
+    def apply(self, a_local, out_dtype=torch.float64, async_op: bool = False, chunks: int = 1):
+        """Full S.A on every rank from this rank's rows ``a_local``.
+
+        ``chunks > 1`` (dense input) pipelines the exchange: SA is computed in
+        contiguous bucket ranges and each range's all-reduce is issued
+        asynchronously as soon as it is written, so NCCL traffic for range k
+        overlaps the computation of range k+1."""
         if a_local.shape[0] != self.row_end - self.row_begin:
             raise ValueError(
                 f"rank {self.rank} expects rows [{self.row_begin}, {self.row_end}), got {a_local.shape[0]} rows"
             )
-        part = self.partial_fn(a_local, out_dtype)
-        work = dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
-        return (part, work) if async_op else part
+        if chunks <= 1:
+            part = self.partial_fn(a_local, out_dtype)
+            work = dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
+            return (part, work) if async_op else part
+        device = a_local.device if isinstance(a_local, torch.Tensor) else torch.device("cpu")
+        out = torch.empty((self.output_dim, a_local.shape[1]), dtype=out_dtype, device=device)
+        works = []
+        for b0, b1 in self.bucket_chunks(chunks):
+            piece = self.partial_fn(a_local, out_dtype, buckets=(b0, b1), out=out)
+            if piece.data_ptr() != out[b0:b1].data_ptr():
+                out[b0:b1].copy_(piece)
+            works.append(dist.all_reduce(out[b0:b1], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        if async_op:
+            return out, works
+        for w in works:
+            w.wait()
+        return out
 
     def descriptor(self) -> dict:
         return {"family": self.family, "n": self.input_dim, "t": self.output_dim, "seed": self.seed}

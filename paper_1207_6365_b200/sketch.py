@@ -360,7 +360,10 @@ class SparseEmbedding(SketchOperator):
         dev_a = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
         return self._apply_dense_device(dev_a, out_t, check_finite).cpu().numpy()
 
-    def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None):
+    def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None, buckets=None):
+        """K3 on a device tensor.  ``buckets=(b0, b1)`` computes only SA rows
+        [b0, b1) (the multi-GPU pipeline reduces finished bucket ranges while
+        the next range is computed)."""
         if a.device != self.device:
             raise ValueError(f"input on {a.device}, operator on {self.device}")
         if a.dim() == 1:
@@ -376,12 +379,16 @@ class SparseEmbedding(SketchOperator):
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
         flag = torch.empty(1, dtype=torch.int32, device=self.device) if check_finite else None
+        b0, b1 = (0, self.output_dim) if buckets is None else (int(buckets[0]), int(buckets[1]))
+        if not (0 <= b0 < b1 <= self.output_dim):
+            raise ValueError(f"bad bucket range {buckets!r}")
         with torch.cuda.device(self.device):
             check(
                 _lib.lib().skt_apply_dense(
-                    _ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim, n, _ptr(a),
-                    _TORCH_TO_SKT[a.dtype], d, lda, _ptr(out), _TORCH_TO_SKT[out.dtype],
-                    out.stride(0) if d > 0 else 1, _ptr(flag), _stream_ptr(self.device),
+                    _ptr(self.plan_indptr) + 8 * b0, _ptr(self.plan_rows), b1 - b0, n, _ptr(a),
+                    _TORCH_TO_SKT[a.dtype], d, lda, _ptr(out) + b0 * out.stride(0) * out.element_size(),
+                    _TORCH_TO_SKT[out.dtype], out.stride(0) if d > 0 else 1, _ptr(flag),
+                    _stream_ptr(self.device),
                 )
             )
         if check_finite and d > 0 and int(flag.item()) != 0:

@@ -46,19 +46,26 @@ def _worker(rank, world, port, n, t, d, seed, kind, q):
         else:
             a = sp.csr_array(sp.random_array((n, d), density=0.2, rng=rng, format="csr"))
 
-        def partial(a_local, out_dtype):
+        def partial(a_local, out_dtype, buckets=None, out=None):
             r0, r1 = op.row_begin, op.row_end
+            if isinstance(a_local, torch.Tensor):
+                a_local = a_local.numpy()
             if kind == "dense":
                 p = O.apply_dense(h[r0:r1], s[r0:r1], t, a_local)
             else:
                 p = O.apply_csr(h[r0:r1], s[r0:r1], t, a_local)
-            return torch.from_numpy(p).to(out_dtype)
+            p = torch.from_numpy(p).to(out_dtype)
+            return p if buckets is None else p[buckets[0] : buckets[1]]
 
         op = ShardedSparseEmbedding(n, t, seed, partial_fn=partial)
         local = a[op.row_begin : op.row_end]
         out = op.apply(local).numpy()
+        full = O.apply(h, s, t, a)
+        if kind == "dense":  # pipelined exchange: bucket ranges reduced as they finish
+            out_c = op.apply(torch.from_numpy(local), chunks=5).numpy()
+            assert np.array_equal(out_c, out)
+            assert op.bucket_chunks(5)[0][0] == 0 and op.bucket_chunks(5)[-1][1] == t
         if rank == 0:
-            full = O.apply(h, s, t, a)
             rel = np.linalg.norm(out - full) / max(np.linalg.norm(full), 1e-300)
             q.put((rel, op.row_begin, op.row_end))
         with pytest.raises(ValueError):

@@ -178,6 +178,20 @@ def test_apply_dense_shapes(dtype, d, rng):
     assert np.array_equal(f32, ref.astype(np.float32))  # one rounding of the exact fp64 sum
 
 
+def test_apply_dense_bucket_ranges(rng):
+    """The multi-GPU pipeline computes SA in bucket ranges: same bits as one launch."""
+    n, t, d = 50_000, 1_003, 32
+    a = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32)).cuda()
+    op = SparseEmbedding(n, t, seed=12)
+    full = op.apply(a)
+    out = torch.empty_like(full)
+    for b0, b1 in [(0, 1), (1, 500), (500, 1002), (1002, 1003)]:
+        op._apply_dense_device(a, torch.float64, out=out, buckets=(b0, b1))
+    assert torch.equal(out, full)
+    with pytest.raises(ValueError):
+        op._apply_dense_device(a, torch.float64, buckets=(5, 5))
+
+
 def test_apply_dense_strided_rows(rng):
     n, t = 1000, 37
     big = torch.from_numpy(rng.standard_normal((n, 40))).cuda()
