@@ -44,7 +44,7 @@ from sketchnla.leverage import _basis_change  # noqa: E402
 from sketchnla.linalg import DEFAULT_TOL, pivoted_qr_rank  # noqa: E402
 from sketchnla.regress import sketch_solve_ls  # noqa: E402
 
-from tests.synth import config1, config2, lev_case  # noqa: E402
+from tests.synth import config1, config2, lev_case, lowrank_case  # noqa: E402
 
 
 def sha(a: np.ndarray) -> str:
@@ -177,6 +177,17 @@ def configs():
     np.savez_compressed(os.path.join(HERE, "lev_case.npz"), probe=probe, scores=scores, sa=sa)
     res["lev"] = {"n": a.shape[0], "d": a.shape[1], "m": m, "k": k, "seed": seed, "rank": rank,
                   "sha_sa": sha(sa), "sha_probe": sha(probe)}
+    # ---- low_rank_approx with explicit sparse-embedding sketches (config-5 shape, scaled)
+    from sketchnla.lowrank import low_rank_approx
+
+    a, k, seed, t_r, t_s = lowrank_case()
+    r_op = RS.make_sparse_embedding(a.shape[1], t_r, 11)
+    s_op = RS.make_sparse_embedding(a.shape[0], t_s, 12)
+    lr = low_rank_approx(a, k, 0.5, seed=seed, r_op=r_op, s_op=s_op)
+    np.savez_compressed(os.path.join(HERE, "lowrank_case.npz"), l=lr.factors.l, d=lr.factors.d,
+                        w=lr.factors.w)
+    res["lowrank"] = {"k": k, "seed": seed, "t_r": t_r, "t_s": t_s, "err": lr.err, "cond_su": lr.cond_su,
+                      "r_op_seed": 11, "s_op_seed": 12, "eps": 0.5}
     with open(os.path.join(HERE, "configs.json"), "w") as f:
         json.dump(res, f, indent=1)
 

@@ -57,6 +57,28 @@ def config2():
     return a, b, SKETCH_SEED
 
 
+def lowrank_case():
+    """Config-5 shaped low-rank case at oracle size: square CSR n = 3,000 with
+    2% density, values (U V^T)_ij + 0.01 N(0,1), U, V ~ N(0,1)^{n x 5};
+    k = 5, column sketch t_r = 20, row sketch t_s = 300."""
+    rng = np.random.default_rng(105)
+    n, r = 3_000, 5
+    u = rng.standard_normal((n, r))
+    v = rng.standard_normal((n, r))
+    a = csr_fixed_nnz(rng, n, n, 60)
+    rows = np.repeat(np.arange(n), 60)
+    a.data = matvec_rows(u[rows], v[a.indices]) + 0.01 * rng.standard_normal(a.nnz)
+    return a, r, 3, 20, 300
+
+
+def matvec_rows(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Row-wise dot products with a fixed summation order (no BLAS)."""
+    acc = x[:, 0] * y[:, 0]
+    for j in range(1, x.shape[1]):
+        acc = acc + x[:, j] * y[:, j]
+    return acc
+
+
 def lev_case():
     """Config-4 shaped leverage case, scaled to oracle size: CSR fp64 n=20,000,
     d=16, 6 random columns per row, 1% of rows fully dense with N(0, 100)

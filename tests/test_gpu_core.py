@@ -383,3 +383,30 @@ def test_leverage_pipeline_matches_reference_pieces():
     # the probe comes from the host QR / inverse (LAPACK: last bits host-dependent)
     assert np.linalg.norm(run.probe - z["probe"]) <= 1e-12 * np.linalg.norm(z["probe"])
     assert np.max(np.abs(run.scores - z["scores"]) / np.abs(z["scores"])) <= 1e-12
+
+
+# ---------------------------------------------------------------- low-rank caller (config-5 shape)
+def test_low_rank_approx_matches_reference():
+    from paper_1207_6365_b200.lowrank import best_rank_k_error_gpu, low_rank_approx
+    from tests import synth
+
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))["lowrank"]
+    z = load("lowrank_case.npz")
+    a, k, seed, t_r, t_s = synth.lowrank_case()
+    r_op = SparseEmbedding(a.shape[1], t_r, cfg["r_op_seed"])
+    s_op = SparseEmbedding(a.shape[0], t_s, cfg["s_op_seed"])
+    res = low_rank_approx(a, k, cfg["eps"], seed=seed, r_op=r_op, s_op=s_op)
+    # sketches are bit-exact; the small SVDs are LAPACK on the host -> 1e-9
+    assert abs(res.err - cfg["err"]) <= 1e-9 * cfg["err"]
+    assert abs(res.cond_su - cfg["cond_su"]) <= 1e-9 * cfg["cond_su"]
+    assert np.max(np.abs(res.factors.d - z["d"])) <= 1e-9 * z["d"][0]
+    for name in ("l", "w"):
+        got, want = getattr(res.factors, name), z[name]
+        sgn = np.sign(np.sum(got * want, axis=0))  # SVD column signs
+        assert np.max(np.abs(got * sgn - want)) <= 1e-7
+    # substitute oracle for Delta_k (randomized subspace iteration) vs the dense SVD
+    dense = a.toarray()
+    sig = np.linalg.svd(dense, compute_uv=False)
+    delta = float(np.sqrt(np.sum(sig[k:] ** 2)))
+    assert abs(best_rank_k_error_gpu(a, k) - delta) <= 1e-6 * delta
+    assert res.err >= delta * (1 - 1e-9)
