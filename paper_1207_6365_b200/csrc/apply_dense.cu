@@ -19,8 +19,14 @@ namespace skt {
 namespace {
 
 constexpr int kThreads = 256;
+// Tuned on config 3 (tools/dense_ceiling.py): software-pipelined gather
+// (batch k+1 in flight while batch k is accumulated), 4 rows per batch,
+// >= 3 resident blocks per SM.
+#ifndef SKT_DENSE_PIPE
+#define SKT_DENSE_PIPE 1
+#endif
 #ifndef SKT_DENSE_MINB
-#define SKT_DENSE_MINB 4
+#define SKT_DENSE_MINB 3
 #endif
 
 template <typename T, int VEC>
@@ -108,6 +114,51 @@ __global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
   const int64_t beg = live ? indptr[bucket] : 0;
   const int64_t end = live ? indptr[bucket + 1] : 0;
   const TIn *acol = a + col;
+#if SKT_DENSE_PIPE
+  // software pipeline: the rows of batch k+1 are in flight while batch k is
+  // accumulated; plan words run one further batch ahead.
+  auto words = [&](int64_t k0, uint32_t(&w)[kUnroll]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) w[u] = (k0 + u < end) ? __ldg(rows + k0 + u) : 0u;
+  };
+  auto gather = [&](int64_t k0, const uint32_t(&w)[kUnroll], V(&v)[kUnroll]) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      v[u] = (active && k0 + u < end)
+                 ? ldstream(reinterpret_cast<const V *>(acol + (int64_t)(w[u] & 0x7fffffffu) * lda))
+                 : V{};
+  };
+  uint32_t wa[kUnroll], wb[kUnroll];
+  V va[kUnroll];
+  words(beg, wa);
+  gather(beg, wa, va);
+  words(beg + kUnroll, wb);
+  for (int64_t k0 = beg; k0 < end; k0 += kUnroll) {
+    V vb[kUnroll];
+    uint32_t wc[kUnroll];
+    gather(k0 + kUnroll, wb, vb);
+    words(k0 + 2 * kUnroll, wc);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (k0 + u < end) {
+        const bool neg = (wa[u] >> 31) != 0;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const TIn x = reinterpret_cast<const TIn *>(&va[u])[k];
+          bad |= nonfinite(x);
+          const double xd = (double)x;
+          acc[k] += neg ? -xd : xd;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      wa[u] = wb[u];
+      va[u] = vb[u];
+      wb[u] = wc[u];
+    }
+  }
+#else
   // plan words of the next kUnroll rows are loaded one iteration ahead, so
   // each iteration waits for one DRAM round trip (the row gather) only
   uint32_t wn[kUnroll];
@@ -144,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
       }
     }
   }
+#endif
   if (active) {
     TOut *o = sa + bucket * ldsa + col;
     if (col + VEC <= d) {
