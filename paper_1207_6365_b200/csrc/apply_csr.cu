@@ -130,6 +130,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32) apply_csr_kernel(
   for (int64_t c = lane; c < d; c += 32) o[c] = (TOut)acc[c];
 }
 
+// SKT_CSR_KERNEL=lane selects the bucket-lane kernel over the tile kernel (A/B).
+inline bool force_lane() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_CSR_KERNEL");
+    return e && e[0] == 'l';
+  }();
+  return on;
+}
+
 template <typename IP, typename IX, typename TV, typename TOut>
 skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
                   uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
@@ -159,7 +168,7 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
     return check_launch(fn);
   }
   // (2) densify-in-shared-memory tiles, warp per bucket (longer rows)
-  if (canon && shift == 0 && d <= kTileMaxD) {
+  if (canon && shift == 0 && d <= kTileMaxD && !force_lane()) {
     const int dp = (int)((d + 1) & ~1LL);
     const int R = (int)std::min<int64_t>(32, tile_bytes<TV>() / ((int64_t)dp * sizeof(TV)));
     const size_t smem = (size_t)(tile_bytes<TV>() + 32 * sizeof(int4)) * kTileWarps;
@@ -172,15 +181,28 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
                (const IX *)aix, (const TV *)av, (int)d, dp, R, (TOut *)sa, ldsa);
     return check_launch(fn);
   }
-  // (3) bucket-lane kernel: one bucket per lane (moderate d)
-  const size_t lane_smem = short_rows ? LaneSmem<IX, TV, 8>::bytes((int)d) : LaneSmem<IX, TV, 16>::bytes((int)d);
-  if (canon && shift == 0 && lane_smem <= 200 * 1024) {
-    const int64_t blocks = ((int64_t)t + 31) / 32;
-    auto k = short_rows ? csr_lane_kernel<IP, IX, TV, TOut, 8> : csr_lane_kernel<IP, IX, TV, TOut, 16>;
-    SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lane_smem), fn);
-    SKT_LAUNCH(k, (unsigned)blocks, 32, lane_smem, stream, pindptr, prow, t, (const IP *)aip,
-               (const IX *)aix, (const TV *)av, (int)d, (TOut *)sa, ldsa);
-    return check_launch(fn);
+  // (3) bucket-lane kernel: BPW buckets per warp, CS lanes (column ranges) per bucket
+  if (canon && shift == 0) {
+    // about 16 warps per SM resident at once: CS = 32 * 2368 / t, power of two in [1, 8]
+    int cs = 1;
+    while (cs < 8 && cs < d && (double)t * cs / 32.0 < 148.0 * 12) cs <<= 1;
+    size_t lane_smem = 0;
+    void (*k)(const int64_t *, const uint32_t *, uint64_t, const IP *, const IX *, const TV *, int, TOut *,
+              int64_t) = nullptr;
+    switch (cs) {
+      case 1: k = csr_lane_kernel<IP, IX, TV, TOut, 1>; lane_smem = LaneSmem<IX, TV, 32>::bytes((int)d); break;
+      case 2: k = csr_lane_kernel<IP, IX, TV, TOut, 2>; lane_smem = LaneSmem<IX, TV, 16>::bytes((int)d); break;
+      case 4: k = csr_lane_kernel<IP, IX, TV, TOut, 4>; lane_smem = LaneSmem<IX, TV, 8>::bytes((int)d); break;
+      default: k = csr_lane_kernel<IP, IX, TV, TOut, 8>; lane_smem = LaneSmem<IX, TV, 4>::bytes((int)d); break;
+    }
+    if (lane_smem <= 200 * 1024) {
+      const int64_t bpw = 32 / cs;
+      const int64_t blocks = ((int64_t)t + bpw - 1) / bpw;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lane_smem), fn);
+      SKT_LAUNCH(k, (unsigned)blocks, 32, lane_smem, stream, pindptr, prow, t, (const IP *)aip,
+                 (const IX *)aix, (const TV *)av, (int)d, (TOut *)sa, ldsa);
+      return check_launch(fn);
+    }
   }
   if (shift != 0)
     return fail(SKT_EINVAL, fn, "non-canonical or wide-d CSR needs the per-bucket plan (shift 0)");

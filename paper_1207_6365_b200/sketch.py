@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import scipy.sparse as sp
@@ -271,7 +272,7 @@ class SparseEmbedding(SketchOperator):
         one warp per group across the chip (148 SMs x 32 warps), group
         accumulators <= 24 KB.  Everything else sweeps the per-bucket plan."""
         m = self.row_end - self.row_begin
-        if not canonical or nnz is None or m == 0 or nnz > 8 * m:
+        if not canonical or nnz is None or m == 0 or nnz > 8 * m or os.environ.get("SKT_CSR_KERNEL") == "lane":
             return 0
         shift, resident = 0, 148 * 32
         while shift < 8 and (self.output_dim >> shift) > resident and (2 << shift) * d * 8 <= 24 * 1024:
