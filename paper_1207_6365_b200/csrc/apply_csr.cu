@@ -189,11 +189,11 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
     size_t lane_smem = 0;
     void (*k)(const int64_t *, const uint32_t *, uint64_t, const IP *, const IX *, const TV *, int, TOut *,
               int64_t) = nullptr;
-    switch (cs) {
-      case 1: k = csr_lane_kernel<IP, IX, TV, TOut, 1>; lane_smem = LaneSmem<IX, TV, 32>::bytes((int)d); break;
-      case 2: k = csr_lane_kernel<IP, IX, TV, TOut, 2>; lane_smem = LaneSmem<IX, TV, 16>::bytes((int)d); break;
-      case 4: k = csr_lane_kernel<IP, IX, TV, TOut, 4>; lane_smem = LaneSmem<IX, TV, 8>::bytes((int)d); break;
-      default: k = csr_lane_kernel<IP, IX, TV, TOut, 8>; lane_smem = LaneSmem<IX, TV, 4>::bytes((int)d); break;
+    switch (cs) {  // 16 (or 32) rows per round: RPB = 16 / buckets-per-warp
+      case 1: k = csr_lane_kernel<IP, IX, TV, TOut, 1, 1>; lane_smem = LaneSmem<IX, TV, 32, 1>::bytes((int)d); break;
+      case 2: k = csr_lane_kernel<IP, IX, TV, TOut, 2, 1>; lane_smem = LaneSmem<IX, TV, 16, 1>::bytes((int)d); break;
+      case 4: k = csr_lane_kernel<IP, IX, TV, TOut, 4, 2>; lane_smem = LaneSmem<IX, TV, 8, 2>::bytes((int)d); break;
+      default: k = csr_lane_kernel<IP, IX, TV, TOut, 8, 4>; lane_smem = LaneSmem<IX, TV, 4, 4>::bytes((int)d); break;
     }
     if (lane_smem <= 200 * 1024) {
       const int64_t bpw = 32 / cs;
