@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import threading
 
 import numpy as np
 import scipy.sparse as sp
@@ -209,6 +210,7 @@ class SparseEmbedding(SketchOperator):
             raise ValueError(f"bad row_range {row_range!r}")
         self.row_begin, self.row_end = r0, r1
         self._bucket = self._sign = self._mat_cache = None
+        self._plan_lock = threading.Lock()
         self._build()
 
     # ---- K1 + K2 ----------------------------------------------------------
@@ -258,13 +260,15 @@ class SparseEmbedding(SketchOperator):
         return indptr, rows, blo, ws
 
     def grouped_plan(self, shift: int):
-        """Plan with rows sorted by bucket group h >> shift (cached per shift)."""
-        if shift not in self._grouped:
-            with torch.cuda.device(self.device):
-                indptr, rows, blo, ws = self._build_plan(shift, _stream_ptr(self.device))
-                self._grouped[shift] = (indptr, rows, blo)
-                self._grouped_ws = ws
-        return self._grouped[shift]
+        """Plan with rows sorted by bucket group h >> shift (cached per shift;
+        built once even when several host threads apply the operator)."""
+        with self._plan_lock:
+            if shift not in self._grouped:
+                with torch.cuda.device(self.device):
+                    indptr, rows, blo, ws = self._build_plan(shift, _stream_ptr(self.device))
+                    self._grouped[shift] = (indptr, rows, blo)
+                    self._grouped_ws = ws
+            return self._grouped[shift]
 
     def csr_group_shift(self, d: int, canonical: bool, nnz: int | None = None) -> int:
         """Plan granularity for the CSR kernels.  Short canonical rows (mean

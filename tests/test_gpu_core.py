@@ -285,6 +285,21 @@ def test_structure_zero_linearity_determinism(rng):
     assert np.array_equal(op.apply(dense), op.apply(sp.csr_array(dense)))
 
 
+def test_concurrent_apply_from_host_threads(rng):
+    """The reference CLI fans apply() over a ThreadPoolExecutor (cli.py:227-231):
+    concurrent calls on one operator give the same bits as serial ones."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    n, t = 20_000, 500
+    op = SparseEmbedding(n, t, seed=4)
+    mats = [rng.standard_normal((n, 8)) for _ in range(6)]
+    mats += [sp.csr_array(sp.random_array((n, 40), density=0.05, rng=rng, format="csr")) for _ in range(6)]
+    serial = [op.apply(m) for m in mats]
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(op.apply, mats))
+    assert all(np.array_equal(x, y) for x, y in zip(serial, par))
+
+
 def test_monte_carlo_unbiased():
     x = np.ones((4, 1))
     total = sum(float(np.sum(make_sparse_embedding(4, 8, seed=seed).apply(x) ** 2)) for seed in range(2000))
