@@ -216,7 +216,10 @@ skt_status launch(const int64_t *indptr, const uint32_t *rows, uint64_t t, const
   const int64_t n_items = (int64_t)t * n_chunks;
   const int64_t warps = (n_items + (32 / G) - 1) / (32 / G);
   const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  constexpr int kUnroll = (sizeof(TIn) * VEC >= 16) ? 4 : 8;
+#ifndef SKT_DENSE_UNROLL8
+#define SKT_DENSE_UNROLL8 8
+#endif
+  constexpr int kUnroll = (sizeof(TIn) * VEC >= 16) ? 4 : SKT_DENSE_UNROLL8;
   SKT_LAUNCH((apply_dense_kernel<TIn, TOut, VEC, G, kUnroll>), (unsigned)blocks, kThreads, 0, stream,
              indptr, rows, n_items, n_chunks, a, d, lda, sa, ldsa, flag);
   return check_launch("skt_apply_dense");
@@ -270,7 +273,10 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
                (int)row_bytes, lda_bytes, (int)d, sa, ldsa, flag);
     return check_launch("skt_apply_dense");
   }
-  if (sizeof(TIn) == 4 && ok(4))
+#ifndef SKT_DENSE_MAXVEC
+#define SKT_DENSE_MAXVEC 4
+#endif
+  if (SKT_DENSE_MAXVEC >= 4 && sizeof(TIn) == 4 && ok(4))
     return dispatch_g<TIn, TOut, (sizeof(TIn) == 4 ? 4 : 2)>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
   if (ok(2)) return dispatch_g<TIn, TOut, 2>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
   return dispatch_g<TIn, TOut, 1>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);

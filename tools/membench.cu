@@ -91,6 +91,40 @@ __global__ void __launch_bounds__(128) bulk_kernel(const char *__restrict__ p, i
   if (acc == 123.456f) out[0] = acc;
 }
 
+// per-warp streams: warp w reads its own contiguous chunk of `chunk` bytes in
+// 512-byte rows, U rows in flight (the access pattern of K3 on an identity plan)
+template <int U>
+__global__ void __launch_bounds__(256) stream_kernel(const float4 *__restrict__ p, int64_t n_float4,
+                                                     int64_t chunk_f4, float *out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t base = warp * chunk_f4;
+  float acc = 0.f;
+  if (base < n_float4) {
+    for (int64_t r = 0; r < chunk_f4; r += 32 * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_nc(p + base + r + u * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+    }
+  }
+  if (acc == 123.456f) out[0] = acc;
+}
+
+extern "C" int mb_stream(const void *p, int64_t n_float4, int64_t chunk_f4, int unroll, float *out,
+                         void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t warps = n_float4 / chunk_f4;
+  const int64_t blocks = (warps * 32 + 255) / 256;
+  switch (unroll) {
+    case 4: stream_kernel<4><<<blocks, 256, 0, st>>>((const float4 *)p, n_float4, chunk_f4, out); break;
+    case 8: stream_kernel<8><<<blocks, 256, 0, st>>>((const float4 *)p, n_float4, chunk_f4, out); break;
+    default: return 1;
+  }
+  return (int)cudaGetLastError();
+}
+
 extern "C" int mb_read(const void *p, int64_t n_float4, int unroll, int blocks, float *out, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   switch (unroll) {

@@ -20,6 +20,11 @@ for u in (4, 8, 16):
     for blocks in (148 * 4, 148 * 8, 148 * 16):
         ms = t(lambda: L.mb_read(ctypes.c_void_p(A.data_ptr()), ctypes.c_int64(n // 4), u, blocks, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
         res[f"ldg_u{u}_b{blocks}"] = round(n * 4 / ms / 1e6, 1)
+for chunk_kb in (128, 32):
+    for u in (4, 8):
+        cf4 = chunk_kb * 1024 // 16
+        ms = t(lambda: L.mb_stream(ctypes.c_void_p(A.data_ptr()), ctypes.c_int64(n // 4), ctypes.c_int64(cf4), u, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
+        res[f"stream_{chunk_kb}k_u{u}"] = round(n * 4 / ms / 1e6, 1)
 for blocks in (148, 148 * 2, 148 * 3):
     ms = t(lambda: L.mb_bulk(ctypes.c_void_p(A.data_ptr()), ctypes.c_int64(n * 4), blocks, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st)))
     res[f"bulk_b{blocks}"] = round(n * 4 / ms / 1e6, 1)
