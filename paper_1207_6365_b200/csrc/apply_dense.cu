@@ -98,7 +98,12 @@ __global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
   constexpr int kGroups = 32 / G;
   const int lane = threadIdx.x & 31;
   const int grp = lane / G, glane = lane % G;
-  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  // persistent warps: grid-stride over work items (no per-block launch /
+  // start-up bubbles between buckets)
+  const int64_t warp0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  bool bad = false;
+  for (int64_t warp = warp0; warp * kGroups < n_items; warp += nwarps) {
   const int64_t item = warp * kGroups + grp;
   const bool live = item < n_items;
   const int64_t bucket = live ? item / n_chunks : 0;
@@ -109,7 +114,6 @@ __global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
   double acc[VEC];
 #pragma unroll
   for (int k = 0; k < VEC; ++k) acc[k] = 0.0;
-  bool bad = false;
 
   const int64_t beg = live ? indptr[bucket] : 0;
   const int64_t end = live ? indptr[bucket + 1] : 0;
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, SKT_DENSE_MINB) apply_dense_kernel(
       for (int k = 0; k < VEC && col + k < d; ++k) o[k] = (TOut)acc[k];
     }
   }
+  }  // persistent loop
   if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 }
 
@@ -215,7 +220,14 @@ skt_status launch(const int64_t *indptr, const uint32_t *rows, uint64_t t, const
   const int64_t n_chunks = (d + G * VEC - 1) / (G * VEC);
   const int64_t n_items = (int64_t)t * n_chunks;
   const int64_t warps = (n_items + (32 / G) - 1) / (32 / G);
-  const int64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+#ifndef SKT_DENSE_BLOCKS_PER_SM
+#define SKT_DENSE_BLOCKS_PER_SM 0  // persistent grids measured slower on config 3
+#endif
+  // persistent grid: SKT_DENSE_BLOCKS_PER_SM resident blocks per SM (0 = one block per 8 items)
+  const int64_t need = (warps * 32 + kThreads - 1) / kThreads;
+  const int64_t blocks = SKT_DENSE_BLOCKS_PER_SM > 0
+                             ? std::min<int64_t>(need, (int64_t)kNumSMs * SKT_DENSE_BLOCKS_PER_SM)
+                             : need;
 #ifndef SKT_DENSE_UNROLL8
 #define SKT_DENSE_UNROLL8 8
 #endif
