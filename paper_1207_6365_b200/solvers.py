@@ -246,6 +246,75 @@ def leverage_scores_sketched(a, m: int, k: int, seed: int, rep: int = 0) -> Leve
     return LeverageRun(scores, rank, sa, probe)
 
 
+def _srht_apply(sa: np.ndarray, t: int, seed: int) -> np.ndarray:
+    """SrhtOperator(n, t, seed).apply (sketch.py:241-302) restated on the host:
+    a thin step on the small sketch (t1 x d) -- not part of the GPU hot path."""
+    n = sa.shape[0]
+    n_pad = 1 << (n - 1).bit_length()
+    sign = np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, 0))).choice(
+        np.array([-1.0, 1.0]), size=n_pad)
+    rows = np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, 1))).integers(0, n_pad, size=t)
+    scale = math.sqrt(n_pad / t) / math.sqrt(n_pad)
+    out = np.zeros((n_pad, sa.shape[1]))
+    out[:n] = sa
+    out *= sign[:, None]
+    h = 1
+    while h < n_pad:  # _fwht (sketch.py:241-252)
+        out = out.reshape(n_pad // (2 * h), 2, h, -1)
+        out = np.stack((out[:, 0] + out[:, 1], out[:, 0] - out[:, 1]), axis=1).reshape(n_pad, -1)
+        h *= 2
+    return scale * out[rows]
+
+
+@dataclass(frozen=True)
+class LeverageScores:
+    """leverage.py:26-32."""
+
+    scores: np.ndarray
+    eps: float
+    repetitions: int
+    seed: int
+    rank: int
+
+
+def approx_leverage_scores(a, eps: float, repetitions: int = 5, seed: int = 0) -> LeverageScores:
+    """leverage.py:50-97 with the sketch (K3/K4) and the fused contraction +
+    row norms (K5) on the GPU; the pivoted QR / SRHT / basis change of the
+    small sketch and the median stay on the host as in the reference."""
+    from .sketch import check_count  # noqa: PLC0415
+
+    eps = check_eps(eps)
+    repetitions = check_count(repetitions, "repetitions")
+    if repetitions % 2 == 0:
+        raise ValueError("repetitions must be odd for a median to amplify")
+    a = as_matrix(a)
+    n, d = a.shape
+    per_rep = np.zeros((repetitions, n))
+    ranks = []
+    t1 = default_sparse_dim(max(d, 1), 0.25)  # default_t1 (leverage.py:100-102)
+    for rep in range(repetitions):
+        sub = np.random.SeedSequence(int(seed), spawn_key=(100 + rep,)).generate_state(3)
+        s = sparse_embedding_or_identity(n, t1, int(sub[0]))
+        sa = np.asarray(s.apply(a))
+        _, _, _, rank = pivoted_qr_rank(sa)
+        if rank == 0:
+            ranks.append(0)
+            continue
+        log_r = math.log(max(rank, 2))
+        t_f = max(rank + 1, math.ceil(40.0 * rank * log_r * log_r))  # _srht_rows (leverage.py:105-107)
+        fsa = sa if t_f >= sa.shape[0] else _srht_apply(sa, t_f, int(sub[1]))
+        n_mat, rank2 = basis_change(fsa)
+        ranks.append(rank2)
+        if rank2 == 0:
+            continue
+        m = max(1, math.ceil(16.0 * math.log(max(n, 2)) / eps**2))
+        probe = n_mat @ gaussian_jl_entries(m, rank2, int(sub[2])).T
+        per_rep[rep] = lev_rownorms(a, probe)
+    rank = int(np.median(ranks)) if ranks else 0
+    return LeverageScores(scores=np.median(per_rep, axis=0), eps=eps, repetitions=repetitions,
+                          seed=int(seed), rank=rank)
+
+
 __all__ = [
     "as_dense",
     "as_csr",

@@ -177,6 +177,14 @@ def configs():
     np.savez_compressed(os.path.join(HERE, "lev_case.npz"), probe=probe, scores=scores, sa=sa)
     res["lev"] = {"n": a.shape[0], "d": a.shape[1], "m": m, "k": k, "seed": seed, "rank": rank,
                   "sha_sa": sha(sa), "sha_probe": sha(probe)}
+    # ---- approx_leverage_scores end to end (sparse embedding + SRHT + JL probe + median)
+    from sketchnla.leverage import approx_leverage_scores
+
+    g5 = np.random.default_rng(55)
+    dense = g5.standard_normal((5000, 6)) * (g5.random((5000, 6)) < 0.5)
+    lv = approx_leverage_scores(sp.csr_array(dense), eps=0.5, repetitions=3, seed=9)
+    np.savez_compressed(os.path.join(HERE, "approx_lev.npz"), a=dense, scores=lv.scores)
+    res["approx_lev"] = {"eps": 0.5, "repetitions": 3, "seed": 9, "rank": lv.rank}
     # ---- low_rank_approx with explicit sparse-embedding sketches (config-5 shape, scaled)
     from sketchnla.lowrank import low_rank_approx
 

@@ -400,6 +400,23 @@ def test_leverage_pipeline_matches_reference_pieces():
     assert np.max(np.abs(run.scores - z["scores"]) / np.abs(z["scores"])) <= 1e-12
 
 
+def test_approx_leverage_scores_end_to_end():
+    """leverage.py:50-97 mirror (GPU sketch + GPU contraction, host QR/SRHT/median)
+    against the reference run on the same input (fp64: 1e-12)."""
+    from paper_1207_6365_b200.solvers import approx_leverage_scores
+
+    cfg = json.load(open(os.path.join(GOLDEN, "configs.json")))["approx_lev"]
+    z = load("approx_lev.npz")
+    res = approx_leverage_scores(sp.csr_array(z["a"]), cfg["eps"], cfg["repetitions"], cfg["seed"])
+    assert res.rank == cfg["rank"]
+    ref = z["scores"]
+    assert np.max(np.abs(res.scores - ref) / np.maximum(np.abs(ref), 1e-300)) <= 1e-10
+    res_d = approx_leverage_scores(z["a"], cfg["eps"], cfg["repetitions"], cfg["seed"])
+    assert np.max(np.abs(res_d.scores - ref) / np.maximum(np.abs(ref), 1e-300)) <= 1e-10
+    with pytest.raises(ValueError):
+        approx_leverage_scores(z["a"], 0.5, repetitions=2)
+
+
 # ---------------------------------------------------------------- low-rank caller (config-5 shape)
 def test_low_rank_approx_matches_reference():
     from paper_1207_6365_b200.lowrank import best_rank_k_error_gpu, low_rank_approx
