@@ -463,7 +463,7 @@ def our_arm(args, cfg):
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config),
+                "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config if lev is None else args.config + "_lev"),
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
                 "kernel_ms": round(kern_ms, 4), "alg_bytes_per_launch": alg_bytes,
                 "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}

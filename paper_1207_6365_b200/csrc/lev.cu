@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "lev_tc.cuh"
+#include "lev_tc2.cuh"
 
 namespace skt {
 namespace {
@@ -23,6 +24,15 @@ inline bool lev_tc_enabled() {
   static const bool on = [] {
     const char *e = getenv("SKT_LEV_TC");
     return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// SKT_LEV_TC2=1 selects the staged, warp-specialised 2xFP16 kernel
+// (lev_tc2.cuh; measured slower than lev_tc.cuh on config 4, kept for A/B).
+inline bool lev_tc2_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_LEV_TC2");
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -133,17 +143,33 @@ template <typename IP, typename IX, typename TV, typename TS>
 skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, const void *av,
                       const double *p, int64_t k, void *scores, cudaStream_t st) {
   static const char *fn = "skt_lev_rownorms_csr";
-  // fp32 values on the tensor cores (3xTF32, tcgen05) when the shape fits
+  // fp32 values on the tensor cores when the shape fits: the staged scaled
+  // 2xFP16 kernel (lev_tc2.cuh, d <= 128, 16-byte aligned arrays), else the
+  // register-staged 3xTF32 kernel (lev_tc.cuh)
   if (std::is_same<TV, float>::value && lev_tc_enabled() && d <= 256 && k >= 8 && k <= 256 && k % 8 == 0) {
-    const int dk = (int)((d + 7) & ~7LL);
-    const size_t smem = lev_tc_smem(dk, (int)k);
+    const T2Layout L = lev_tc2_layout((int)d, (int)k, (int)sizeof(IX));
+    const bool aligned = ((uintptr_t)aip % 16 == 0) && ((uintptr_t)aix % 16 == 0) && ((uintptr_t)av % 16 == 0);
+    if (lev_tc2_enabled() && L.nst > 0 && aligned) {
+      auto kern = lev_tc2_kernel<IP, IX, TS>;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem), fn);
+      const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
+      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)kNumSMs);
+      SKT_LAUNCH(kern, (unsigned)blocks, kT2Threads, L.smem, st, n, (int)d, (const IP *)aip,
+                 (const IX *)aix, (const float *)av, p, (int)k, (TS *)scores, L);
+      return check_launch(fn);
+    }
+    const int dk8 = (int)((d + 7) & ~7LL);  // K of the MMA chain
+    const size_t smem = lev_tc_smem(dk8, (int)k);
     if (smem <= 200 * 1024) {
       auto kern = lev_tc_kernel<IP, IX, TS>;
       SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
       const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
-      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / smem));
+      // resident CTAs per SM: bounded by shared memory and by the 512 TMEM
+      // columns (a CTA's tcgen05.alloc would otherwise wait forever)
+      const size_t by_tmem = 512 / lev_tc_cols((int)k);
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>(4, by_tmem), (220 * 1024) / smem));
       const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm);
-      SKT_LAUNCH(kern, (unsigned)blocks, kTcThreads, smem, st, n, (int)d, dk, (const IP *)aip,
+      SKT_LAUNCH(kern, (unsigned)blocks, kTcThreads, smem, st, n, (int)d, dk8, (const IP *)aip,
                  (const IX *)aix, (const float *)av, p, (int)k, (TS *)scores);
       return check_launch(fn);
     }

@@ -65,6 +65,9 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+// TMEM columns a CTA allocates for a k-wide accumulator
+__host__ __device__ inline uint32_t lev_tc_cols(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256; }
+
 template <typename IP, typename IX, typename TS>
 __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, int dk,
                                                             const IP *__restrict__ aip,
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
     *(float *)((unsigned char *)p_lo + off) = lo;
   }
   if (warp == 0) {
-    const uint32_t ncols = k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256;
+    const uint32_t ncols = lev_tc_cols(k);
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      tc_smem_u32(&tmem_base)),
                  "r"(ncols));
@@ -130,7 +133,29 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
   // gl and gl + 8 of each row (rows of <= 16 nonzeros complete here)
   int pc[E];
   float pv[E];
+  // the tail (nonzeros 16..79) of the warp's first long row also goes in
+  // flight with the tile, so a dense row does not put a dependent load round
+  // trip inside the densify phase (the whole CTA would wait on it)
+  int lr = -1, lc[2];
+  float lv[2];
   auto load_data = [&](int64_t rs, int len) {
+    {
+      const uint32_t lm = __ballot_sync(0xffffffffu, len > 2 * G);
+      lr = lm ? __ffs(lm) - 1 : -1;
+      lc[0] = lc[1] = -1;
+      if (lm) {
+        const int64_t rs_r = __shfl_sync(0xffffffffu, rs, lr);
+        const int len_r = __shfl_sync(0xffffffffu, len, lr);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = 2 * G + lane + 32 * j;
+          if (q < len_r) {
+            lc[j] = (int)__ldg(aix + rs_r + q);
+            lv[j] = __ldg(av + rs_r + q);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < E / 2; ++i) {
       const int r = i * S + g;
@@ -164,15 +189,58 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
   for (; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * kTcRows;
     // ---- densify the staged nonzeros (3xTF32 split)
+    // column order check: a non-increasing pair (duplicate / unsorted row)
+    // marks the tile dirty -> rebuilt below one thread per row
+    bool dirty = false;
+#pragma unroll
+    for (int i = 0; i < E / 2; ++i) {
+      const int p0 = __shfl_up_sync(0xffffffffu, pc[2 * i], 1, G);      // entry gl - 1
+      const int p7 = __shfl_sync(0xffffffffu, pc[2 * i], G - 1, G);     // entry 7
+      const int p1 = __shfl_up_sync(0xffffffffu, pc[2 * i + 1], 1, G);  // entry gl + 7
+      if (gl > 0 && pc[2 * i] >= 0) dirty |= pc[2 * i] <= p0;
+      if (pc[2 * i + 1] >= 0) dirty |= pc[2 * i + 1] <= (gl > 0 ? p1 : p7);
+    }
 #pragma unroll
     for (int i = 0; i < E; ++i)
       if (pc[i] >= 0) put(warp * 32 + (i / 2) * S + g, pc[i], pv[i]);
+    if (lr >= 0) {
+      const int64_t rs_r = __shfl_sync(0xffffffffu, rs_c, lr);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (lc[j] >= 0) {
+          dirty |= lc[j] <= (int)__ldg(aix + rs_r + 2 * G + lane + 32 * j - 1);
+          put(warp * 32 + lr, lc[j], lv[j]);
+        }
+    }
     const uint32_t longm = __ballot_sync(0xffffffffu, len_c > 2 * G);
-    for (uint32_t m = longm; m; m &= m - 1) {  // rows with > 16 nonzeros (whole warp)
+    for (uint32_t m = longm; m; m &= m - 1) {  // rest of the rows with > 16 nonzeros (whole warp)
       const int r = __ffs(m) - 1;
       const int64_t rs_r = __shfl_sync(0xffffffffu, rs_c, r);
       const int len_r = __shfl_sync(0xffffffffu, len_c, r);
-      for (int q = 2 * G + lane; q < len_r; q += 32) put(warp * 32 + r, (int)__ldg(aix + rs_r + q), __ldg(av + rs_r + q));
+      for (int q = (r == lr ? 2 * G + 64 : 2 * G) + lane; q < len_r; q += 32) {
+        const int c = (int)__ldg(aix + rs_r + q);
+        dirty |= c <= (int)__ldg(aix + rs_r + q - 1);
+        put(warp * 32 + r, c, __ldg(av + rs_r + q));
+      }
+    }
+    if (__syncthreads_or(dirty)) {
+      // rebuild: clear, then one thread per row in entry order, summing
+      // duplicates before the split (scipy's a @ probe semantics)
+      for (uint32_t i = tid; i < 2 * a_bytes / 16; i += kTcThreads) ((uint4 *)smem)[i] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      const int64_t r = row0 + tid;
+      if (r < n) {
+        const int64_t rb = (int64_t)aip[r], re = (int64_t)aip[r + 1];
+        for (int64_t q = rb; q < re; ++q) {
+          const uint32_t off = tc_off(tid, (int)aix[q], kTcRows);
+          float *h = (float *)((unsigned char *)a_hi + off);
+          float *l = (float *)((unsigned char *)a_lo + off);
+          const float v = av[q] + (*h + *l);
+          const float hv = tf32_hi(v);
+          *h = hv;
+          *l = tf32_hi(v - hv);
+        }
+      }
     }
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -263,7 +331,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
   }
   __syncthreads();
   if (warp == 0) {
-    const uint32_t ncols = k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256;
+    const uint32_t ncols = lev_tc_cols(k);
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
   }
 }

@@ -368,7 +368,8 @@ def test_lev_rownorms_golden():
 
 
 @pytest.mark.parametrize("n,d,k,density", [(20_000, 64, 32, 0.26), (5_000, 16, 8, 0.5), (3_001, 100, 40, 0.1),
-                                           (4_000, 256, 256, 0.05), (1_000, 8, 16, 1.0)])
+                                           (4_000, 256, 256, 0.05), (1_000, 8, 16, 1.0),
+                                           (2_000, 200, 32, 0.5)])  # every row long
 def test_lev_tensor_core_3xtf32(n, d, k, density, rng):
     """fp32 CSR runs on tcgen05 (3xTF32): scores within 1e-5 of the fp64 oracle."""
     from paper_1207_6365_b200.solvers import lev_rownorms
@@ -383,6 +384,74 @@ def test_lev_tensor_core_3xtf32(n, d, k, density, rng):
     nz = ref > 0
     assert np.all(got[~nz] == 0)
     assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-5
+
+
+@pytest.mark.parametrize("d", [64, 128])  # 64: staged v2 kernel, 128: register-staged v1
+def test_lev_tensor_core_noncanonical_rows(d, rng):
+    """Duplicate and unsorted column indices are summed like scipy's a @ probe
+    (the dirty-tile rebuild), on both tensor-core kernels."""
+    from paper_1207_6365_b200.solvers import lev_rownorms
+
+    n, k = 3_000, 32
+    counts = rng.integers(0, 40, size=n)
+    indptr = np.concatenate([[0], np.cumsum(counts)])
+    indices = np.concatenate([np.sort(rng.choice(d, size=c, replace=False)) for c in np.minimum(counts, d)])
+    indices = indices.astype(np.int32)
+    # every 7th row: duplicates (same column repeated); every 11th: reversed order
+    for r in range(0, n, 7):
+        b, e = indptr[r], indptr[r + 1]
+        if e - b >= 3:
+            indices[b + 1] = indices[b]
+            indices[e - 1] = indices[b]
+    for r in range(3, n, 11):
+        b, e = indptr[r], indptr[r + 1]
+        indices[b:e] = indices[b:e][::-1].copy()
+    vals = rng.standard_normal(indptr[-1]).astype(np.float32)
+    a = sp.csr_array((vals, indices, indptr), shape=(n, d))
+    assert not a.has_canonical_format
+    probe = rng.standard_normal((d, k)) / np.sqrt(k)
+    ref = O.lev_rownorms_csr(a, probe)
+    got = lev_rownorms(a, probe)
+    nz = ref > 1e-12
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-5
+    assert np.all(np.abs(got[~nz]) <= 1e-6)
+
+
+_TC2_SCRIPT = r"""
+import sys, numpy as np, scipy.sparse as sp
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_1207_6365_b200.solvers import lev_rownorms
+rng = np.random.default_rng(7)
+worst = 0.0
+for n, d, k, dens in [(20000, 64, 32, 0.26), (3001, 100, 40, 0.1), (5000, 16, 8, 0.5), (2000, 128, 128, 0.3)]:
+    a = sp.csr_array(sp.random_array((n, d), density=dens, rng=rng, format="csr"), dtype=np.float32).tolil()
+    a[5, :] = rng.standard_normal(d).astype(np.float32) * 1e3   # long row, large scale
+    a[9, :3] = np.float32(1e-30)                                # tiny row
+    a = sp.csr_array(a, dtype=np.float32)
+    p = rng.standard_normal((d, k)) / np.sqrt(k)
+    ref = O.lev_rownorms_csr(a, p)
+    got = lev_rownorms(a, p)
+    nz = ref > 0
+    assert np.all(got[~nz] == 0)
+    worst = max(worst, float(np.max(np.abs(got[nz] - ref[nz]) / ref[nz])))
+print(worst)
+"""
+
+
+def test_lev_staged_fp16_kernel():
+    """The opt-in staged 2xFP16 kernel (SKT_LEV_TC2=1, lev_tc2.cuh), run in a
+    child process (the selector is read once per process): 1e-5 vs the oracle,
+    incl. per-row scaling extremes."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKT_LEV_TC2="1")
+    out = subprocess.run([sys.executable, "-c", _TC2_SCRIPT, root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-5
 
 
 def test_leverage_pipeline_matches_reference_pieces():
