@@ -134,6 +134,18 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else t.data_ptr()
 
 
+def _host(t: torch.Tensor) -> torch.Tensor:
+    """Device result -> a new host tensor in page-locked memory (torch's caching
+    host allocator): the read-back runs at PCIe speed instead of the ~2 GB/s
+    of a copy into freshly faulted pageable pages (15 ms for config 3's SA)."""
+    try:
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    except RuntimeError:  # page-locked memory exhausted
+        return t.cpu()
+    out.copy_(t)
+    return out
+
+
 class SketchOperator:
     """Duck-typed protocol of the reference (sketch.py:97-119)."""
 
@@ -338,11 +350,11 @@ class SparseEmbedding(SketchOperator):
                     parts = tuple(x.to(self.device, non_blocking=True) for x in parts)
                 res = self._apply_csr_device(*parts, a.shape[1], out_t, canonical=False,
                                              deterministic=deterministic)
-                return res if a.is_cuda else res.cpu()
+                return res if a.is_cuda else _host(res)
             if a.is_cuda:
                 return self._apply_dense_device(a, out_t, check_finite)
             dev_a = a.to(self.device, non_blocking=a.is_pinned())
-            return self._apply_dense_device(dev_a, out_t, check_finite).cpu()
+            return _host(self._apply_dense_device(dev_a, out_t, check_finite))
         out_t = torch.float64 if out_dtype is None else out_dtype
         if sp.issparse(a):
             m = sp.csr_array(a)
@@ -353,8 +365,8 @@ class SparseEmbedding(SketchOperator):
             ip = torch.from_numpy(np.ascontiguousarray(m.indptr)).to(dev)
             ix = torch.from_numpy(np.ascontiguousarray(m.indices)).to(dev)
             vv = torch.from_numpy(np.ascontiguousarray(m.data)).to(dev)
-            return self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical,
-                                          deterministic=deterministic).cpu().numpy()
+            return _host(self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical,
+                                                deterministic=deterministic)).numpy()
         arr = np.asarray(a)
         if arr.dtype not in (np.float32, np.float64):
             arr = arr.astype(np.float64)
@@ -363,7 +375,7 @@ class SparseEmbedding(SketchOperator):
         if arr.ndim != 2:
             raise ValueError(f"matrix must be 2-D, got shape {arr.shape}")
         dev_a = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
-        return self._apply_dense_device(dev_a, out_t, check_finite).cpu().numpy()
+        return _host(self._apply_dense_device(dev_a, out_t, check_finite)).numpy()
 
     def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None, buckets=None):
         """K3 on a device tensor.  ``buckets=(b0, b1)`` computes only SA rows
@@ -493,8 +505,8 @@ class SparseEmbedding(SketchOperator):
             if n_rows > 0 and int(flag.item()) != 0:
                 raise ValueError("matrix contains non-finite entries")
         if to_numpy:
-            return y.cpu().numpy()
-        return y if (isinstance(a, torch.Tensor) and a.is_cuda) else y.cpu()
+            return _host(y).numpy()
+        return y if (isinstance(a, torch.Tensor) and a.is_cuda) else _host(y)
 
 
 class ComposedSketch(SketchOperator):

@@ -27,6 +27,7 @@ from .sketch import (
     SparseEmbedding,
     _ITYPE,
     _TORCH_TO_SKT,
+    _host,
     _ptr,
     _stream_ptr,
     check_eps,
@@ -217,8 +218,8 @@ def lev_rownorms(a, probe, device=None, out_dtype=torch.float64):
             if x.shape[0] > 0 and int(flag.item()) != 0:
                 raise ValueError("matrix contains non-finite entries")
     if host:
-        return out.cpu().numpy()
-    return out if a.is_cuda else out.cpu()
+        return _host(out).numpy()
+    return out if a.is_cuda else _host(out)
 
 
 @dataclass(frozen=True)
