@@ -28,6 +28,7 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+L2_FLUSH_BELOW = 4 * 126 * 2**20  # inputs below 4x the 126 MB L2 get an L2 flush per step
 sys.path.insert(0, ROOT)
 
 METRIC = "CountSketch S·A nonzeros/sec and % of HBM roofline at 1/2/4/8 B200"
@@ -41,7 +42,7 @@ CONFIGS = {
     "c4": dict(kind="csr", n=4_194_304, d=64, m=16_384, dtype="f32", per_row=16, dense_frac=0.01, seed=1,
                workload="config4: CSR fp32 4194304x64, 16 nnz/row + 1% dense rows N(0,100), m=16384"),
     "c5": dict(kind="csr", n=262_144, d=262_144, m=400, dtype="f32", per_row=262, lowrank=10, seed=1,
-               fast=True,
+               fast=True, shard="bucket",
                workload="config5: CSR fp32 262144x262144, 262 nnz/row (0.1%), values (U V^T)_ij + 0.01 N, "
                         "rank 10; m=400 row sketch (fast mode: unordered fp32 atomics)"),
 }
@@ -117,6 +118,34 @@ def peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def gather_ceiling_ms(rows: int, seg_bytes):
+    """Time to gather `rows` x (one segment of each size in seg_bytes) at random
+    offsets, at the segment rates measured by tools/gather_bench.cu (log-linear
+    interpolation; segments below 16 B cost one 16 B request)."""
+    import math
+
+    p = os.path.join(ROOT, "profiles", "r01_gather_ceiling.json")
+    try:
+        with open(p) as f:
+            tab = {int(k): float(v) for k, v in json.load(f)["unaligned"].items()}
+    except Exception:
+        return None
+    sizes = sorted(tab)
+    rate = {s: tab[s] * 1e9 / s for s in sizes}  # segments per second
+    t = 0.0
+    for b in seg_bytes:
+        s = min(max(b, sizes[0]), sizes[-1])
+        lo = max(x for x in sizes if x <= s)
+        hi = min(x for x in sizes if x >= s)
+        if lo == hi:
+            r = rate[lo]
+        else:
+            f = (math.log2(s) - math.log2(lo)) / (math.log2(hi) - math.log2(lo))
+            r = math.exp((1 - f) * math.log(rate[lo]) + f * math.log(rate[hi]))
+        t += rows / r
+    return 1e3 * t
 
 
 def traffic_for(cfg_name: str):
@@ -337,7 +366,11 @@ def our_arm(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n, d, m = cfg["n"], cfg["d"], cfg["m"]
-    r0, r1 = rank * n // world, (rank + 1) * n // world
+    # config 5 at N > 1: bucket ownership -- every rank holds the
+    # whole input and computes only its SA rows [b0, b1); no collective
+    bucket_mode = world > 1 and cfg.get("shard") == "bucket" and args.kernel == "sa"
+    r0, r1 = (0, n) if bucket_mode else (rank * n // world, (rank + 1) * n // world)
+    b0, b1 = (rank * m // world, (rank + 1) * m // world) if bucket_mode else (0, m)
     sa_dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
 
     # ---- inputs resident in HBM
@@ -358,6 +391,13 @@ def our_arm(args, cfg):
     tb1.record()
     torch.cuda.synchronize()
     build_ms = tb0.elapsed_time(tb1)
+    if bucket_mode:  # this rank's work: the rows hashed into its buckets
+        gptr, grows, _ = op.grouped_plan(0)
+        p0, p1 = int(gptr[b0]), int(gptr[b1])
+        mine = (grows[p0:p1] & 0x7FFFFFFF).long()
+        lens = (ip[1:] - ip[:-1]).long()
+        nnz_local = int(lens[mine].sum())
+        in_bytes = nnz_local * (vv.element_size() + 4) + (p1 - p0) * 2 * ip.element_size()
 
     SA = torch.empty((m, d), dtype=sa_dt, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -386,7 +426,8 @@ def our_arm(args, cfg):
             op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
         else:
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
-                                 deterministic=not cfg.get("fast", False))
+                                 deterministic=not cfg.get("fast", False),
+                                 buckets=(b0, b1) if bucket_mode else None)
 
     # N > 1, dense: pipelined exchange -- SA is computed in contiguous bucket
     # ranges and each range is all-reduced (async, NCCL stream) while the next
@@ -399,9 +440,9 @@ def our_arm(args, cfg):
             kev[0].record(stream)
         if pipelined:
             works = []
-            for b0, b1 in ranges:
-                op._apply_dense_device(A, sa_dt, check_finite=False, out=SA, buckets=(b0, b1))
-                works.append(dist.all_reduce(SA[b0:b1], async_op=True))
+            for c0, c1 in ranges:
+                op._apply_dense_device(A, sa_dt, check_finite=False, out=SA, buckets=(c0, c1))
+                works.append(dist.all_reduce(SA[c0:c1], async_op=True))
             if kev is not None:
                 kev[1].record(stream)
             for w in works:
@@ -410,15 +451,22 @@ def our_arm(args, cfg):
         apply_once()
         if kev is not None:
             kev[1].record(stream)
-        if world > 1 and lev is None:
+        if world > 1 and lev is None and not bucket_mode:
             dist.all_reduce(SA)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
+    # inputs that fit in L2 (configs 1, 2): L2 is flushed before every step by
+    # writing a 512 MB buffer, and the steps are timed individually (events
+    # around each step only) so the flush is not counted
+    flush_l2 = in_bytes < L2_FLUSH_BELOW
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
+
     def timed_region():
         kevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        sevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
@@ -427,13 +475,18 @@ def our_arm(args, cfg):
         with ClockSampler(local) as clk:
             e0.record(stream)
             for i in range(args.steps):
+                if flush_l2:
+                    flush_buf.fill_(i & 0xFF)
+                    sevs[i][0].record(stream)
                 step(kevs[i])
+                if flush_l2:
+                    sevs[i][1].record(stream)
             e1.record(stream)
             torch.cuda.synchronize()
         launches = launch_count() - lc0
         if world > 1:
             dist.barrier()
-        total_ms = e0.elapsed_time(e1)
+        total_ms = sum(a.elapsed_time(b) for a, b in sevs) if flush_l2 else e0.elapsed_time(e1)
         kern_ms = sum(a.elapsed_time(b) for a, b in kevs) / args.steps
         return total_ms, kern_ms, launches, clk
 
@@ -459,7 +512,7 @@ def our_arm(args, cfg):
     value = nnz_total / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (this rank's apply launch)
-    alg_bytes = in_bytes + (m * d * SA.element_size() if lev is None else (r1 - r0) * 8)
+    alg_bytes = in_bytes + ((b1 - b0) * d * SA.element_size() if lev is None else (r1 - r0) * 8)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     peak, peak_src = peak_hbm()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -467,6 +520,18 @@ def our_arm(args, cfg):
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
                 "kernel_ms": round(kern_ms, 4), "alg_bytes_per_launch": alg_bytes,
                 "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}
+    if cfg["kind"] == "csr" and lev is None and not cfg.get("fast"):
+        # CSR S.A reads every row's (indptr pair, index segment, value segment)
+        # in bucket order = random rows: its ceiling is the random-segment
+        # gather rate measured by tools/gather_bench.cu, not streaming HBM
+        rows_local = r1 - r0
+        per_row = nnz_local / max(rows_local, 1)
+        gc = gather_ceiling_ms(rows_local, [8.0, per_row * ix.element_size(), per_row * vv.element_size()])
+        if gc is not None:
+            roofline["gather_ceiling"] = {
+                "ms": round(gc, 4), "frac": round(gc / kern_ms, 4),
+                "model": "per row: 8 B indptr pair + index segment + value segment at random offsets, each at "
+                         "the measured random-segment rate for its size (profiles/r01_gather_ceiling.json)"}
 
     # ---- end to end through the public API, host buffers
     e2e = None
@@ -510,8 +575,10 @@ def our_arm(args, cfg):
         "config": {"workload": cfg["workload"], "n": n, "d": d, "m": m, "input_dtype": cfg["dtype"],
                    "sa_dtype": "f32" if sa_dt == torch.float32 else "f64",
                    "accumulate": "fp64, ascending row order (bit-identical to the reference)",
-                   "l2": "inputs larger than L2 (no flush needed)",
-                   "parallelism": f"row-shard x{world}" + (
+                   "l2": ("L2 flushed before every step (512 MB write, outside the per-step events)" if flush_l2
+                          else "inputs larger than L2 (no flush needed)"),
+                   "parallelism": (f"bucket-ownership x{world}: rank owns SA rows [{b0}, {b1}), whole input on "
+                                   "every rank, no collective") if bucket_mode else f"row-shard x{world}" + (
                        (f" + NCCL all-reduce of m x d partials, pipelined over {args.chunks} bucket ranges"
                         if pipelined else " + NCCL all-reduce of m x d partials") if world > 1 else "")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -117,7 +117,11 @@ skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t
  * SKT_CSR_CANONICAL: no duplicate column inside a row) with narrow d runs the
  * grouped sweep kernel for any shift, otherwise a shift-0 plan is required.
  * CSR arrays of A may use int32 or int64 indptr / indices; values f32 or f64;
- * nnz = number of stored entries (a_indptr[n]). */
+ * nnz = number of stored entries (a_indptr[n]).
+ * Bucket ranges (K3 and K4, e.g. bucket-ownership sharding across GPUs): SA
+ * rows [b0, b1) alone are computed by passing indptr + b0 (shift-0 plan; a
+ * grouped plan: indptr + (b0 >> shift) with b0 a multiple of 2^shift),
+ * t = b1 - b0 and sa + b0 * ldsa; the rows / blo arrays are shared. */
 skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, const uint8_t *blo,
                          int32_t shift, uint64_t t, int64_t n, const void *a_indptr,
                          skt_itype indptr_type, const void *a_indices, skt_itype index_type,

@@ -171,7 +171,7 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
   if (canon && shift == 0 && d <= kTileMaxD && !force_lane()) {
     const int dp = (int)((d + 1) & ~1LL);
     const int R = (int)std::min<int64_t>(32, tile_bytes<TV>() / ((int64_t)dp * sizeof(TV)));
-    const size_t smem = (size_t)(tile_bytes<TV>() + 32 * sizeof(int4)) * kTileWarps;
+    const size_t smem = (size_t)tile_slice_bytes<TV>() * kTileWarps;
     const int64_t blocks = ((int64_t)t + kTileWarps - 1) / kTileWarps;
     const int chunks = (int)((d + 63) / 64);
     auto k = chunks <= 1 ? csr_tile_kernel<IP, IX, TV, TOut, 1>

@@ -9,10 +9,17 @@
 // additions run over the bucket's rows in ascending order; absent entries add
 // +0.0, an exact identity (the accumulator is never -0.0: it starts at +0.0 and
 // x + y = -0.0 only if both are -0.0), so the result is bit-identical to the
-// reference's bincount.  The row descriptors of batch b+1 and the plan words of
-// batch b+2 are in flight while batch b is gathered and accumulated; a batch's
-// nonzeros are fetched G lanes per row (G = 4/8/16 by the batch's longest row)
-// with all loads issued before the tile stores.
+// reference's bincount.
+//
+// Software pipeline (three batches deep): while batch b is scattered,
+// accumulated and re-zeroed, the nonzeros of batch b+1 are already in flight
+// into registers, the row descriptors (indptr pairs) of batch b+2 and the plan
+// words of batch b+3.  A batch's nonzeros are fetched G lanes per row (G =
+// 4/8/16 by the batch's longest row); the first G of every row are prefetched,
+// longer rows' tails are fetched by the whole warp when the batch is scattered.
+// The random row order makes this kernel request-rate bound (the index and
+// value segments of a row are ~64 B at arbitrary offsets): the ceiling is the
+// same access pattern without arithmetic, tools/gather_bench.cu.
 #pragma once
 
 #include <type_traits>
@@ -24,21 +31,22 @@ namespace {
 
 constexpr int kTileWarps = 4;
 constexpr int kTileMaxD = 256;
+constexpr int kTileDescSlots = 2;  // double-buffered batch descriptors
 
 template <typename TV>
 __host__ __device__ constexpr int tile_bytes() { return sizeof(TV) == 4 ? 8192 : 12288; }
+template <typename TV>
+__host__ __device__ constexpr int tile_slice_bytes() {
+  return tile_bytes<TV>() + kTileDescSlots * 32 * (int)sizeof(int4);
+}
 
-// Phase 1 of a batch: the first G nonzeros of every row, G lanes per row, all
-// loads issued before the tile stores.  Row descriptors come from shared
-// memory (broadcast).  Returns nothing; entries beyond G are left to phase 2.
+// The first G nonzeros of every row of a batch into registers, G lanes per
+// row; row descriptors from shared memory (broadcast).
 template <int G, typename IX, typename TV>
-__device__ __forceinline__ void scatter_rows(const int4 *__restrict__ desc, int nrows,
-                                             const IX *__restrict__ aix,
-                                             const TV *__restrict__ av, TV *tile, int dp,
-                                             int lane, IX (&cc)[16]) {
+__device__ __forceinline__ void load_rows(const int4 *__restrict__ desc, int nrows, const IX *__restrict__ aix,
+                                          const TV *__restrict__ av, int lane, IX (&cc)[16], TV (&vv)[16]) {
   constexpr int S = 32 / G;
   const int g = lane / G, gl = lane % G;
-  TV vv[G];
 #pragma unroll
   for (int i = 0; i < G; ++i) {
     const int r = i * S + g;
@@ -52,6 +60,13 @@ __device__ __forceinline__ void scatter_rows(const int4 *__restrict__ desc, int 
       }
     }
   }
+}
+
+template <int G, typename IX, typename TV>
+__device__ __forceinline__ void store_rows(const int4 *__restrict__ desc, TV *tile, int dp, int lane,
+                                           const IX (&cc)[16], const TV (&vv)[16]) {
+  constexpr int S = 32 / G;
+  const int g = lane / G;
 #pragma unroll
   for (int i = 0; i < G; ++i) {
     const int r = i * S + g;
@@ -60,8 +75,7 @@ __device__ __forceinline__ void scatter_rows(const int4 *__restrict__ desc, int 
 }
 
 template <int G, typename IX, typename TV>
-__device__ __forceinline__ void unscatter_rows(const int4 *__restrict__ desc, int nrows,
-                                               TV *tile, int dp, int lane, const IX (&cc)[16]) {
+__device__ __forceinline__ void unscatter_rows(TV *tile, int dp, int lane, const IX (&cc)[16]) {
   constexpr int S = 32 / G;
   const int g = lane / G;
 #pragma unroll
@@ -69,8 +83,10 @@ __device__ __forceinline__ void unscatter_rows(const int4 *__restrict__ desc, in
     if (cc[i] != (IX)-1) tile[(i * S + g) * dp + (int)cc[i]] = (TV)0;
 }
 
+__device__ __forceinline__ int tile_g(int lmax) { return lmax <= 4 ? 4 : lmax <= 8 ? 8 : 16; }
+
 template <typename IP, typename IX, typename TV, typename TOut, int kChunks>
-__global__ void __launch_bounds__(kTileWarps * 32, 6) csr_tile_kernel(
+__global__ void __launch_bounds__(kTileWarps * 32, 4) csr_tile_kernel(
     const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
     const IP *__restrict__ aip, const IX *__restrict__ aix, const TV *__restrict__ av, int d,
     int dp, int R, TOut *__restrict__ sa, int64_t ldsa) {
@@ -79,9 +95,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, 6) csr_tile_kernel(
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t bucket = (int64_t)blockIdx.x * kTileWarps + w;
   if (bucket >= (int64_t)t) return;
-  unsigned char *slice = smem_raw + (size_t)w * (tile_bytes<TV>() + 32 * sizeof(int4));
-  int4 *desc = (int4 *)slice;  // per row of the batch: rs lo, rs hi, len, neg
-  TV *tile = (TV *)(slice + 32 * sizeof(int4));
+  unsigned char *slice = smem_raw + (size_t)w * tile_slice_bytes<TV>();
+  int4 *descs = (int4 *)slice;  // [slot][row of the batch]: rs lo, rs hi, len, neg
+  TV *tile = (TV *)(slice + kTileDescSlots * 32 * sizeof(int4));
   for (int i = lane; i < R * dp; i += 32) tile[i] = (TV)0;
 
   double acc[kChunks][2];
@@ -89,61 +105,88 @@ __global__ void __launch_bounds__(kTileWarps * 32, 6) csr_tile_kernel(
   for (int k = 0; k < kChunks; ++k) acc[k][0] = acc[k][1] = 0.0;
 
   const int64_t beg = pindptr[bucket], end = pindptr[bucket + 1];
-  // software pipeline: descriptors of batch b+1 and the plan words of batch
-  // b+2 are in flight while batch b is gathered and accumulated.
-  uint32_t w_cur = (lane < R && beg + lane < end) ? __ldg(prow + beg + lane) : 0u;
-  int64_t rs_cur = 0;
-  int len_cur = 0;
-  if (lane < R && beg + lane < end) {
-    const int64_t row = w_cur & 0x7fffffffu;
-    rs_cur = (int64_t)aip[row];
-    len_cur = (int)((int64_t)aip[row + 1] - rs_cur);
-  }
-  uint32_t w_nxt = (lane < R && beg + R + lane < end) ? __ldg(prow + beg + R + lane) : 0u;
+  auto plan_word = [&](int64_t k0) -> uint32_t {
+    return (lane < R && k0 + lane < end) ? __ldg(prow + k0 + lane) : 0u;
+  };
+  auto row_desc = [&](int64_t k0, uint32_t wd, int64_t &rs, int &len) {
+    rs = 0;
+    len = 0;
+    if (lane < R && k0 + lane < end) {
+      const int64_t row = wd & 0x7fffffffu;
+      rs = (int64_t)aip[row];
+      len = (int)((int64_t)aip[row + 1] - rs);
+    }
+  };
+  // publish a batch's descriptors (lane r = row r) into a slot; returns G
+  auto publish = [&](int slot, int64_t k0, int64_t rs, int len, uint32_t wd) -> int {
+    const int nrows = (int)((end - k0) < R ? (end - k0) : R);
+    if (lane < nrows) descs[slot * 32 + lane] = make_int4((int)(uint32_t)rs, (int)(rs >> 32), len, (int)(wd >> 31));
+    return tile_g(__reduce_max_sync(0xffffffffu, lane < nrows ? len : 0));
+  };
+  auto load_sw = [&](int G, const int4 *dsc, int nrows, IX (&c)[16], TV (&v)[16]) {
+    if (G == 4)
+      load_rows<4>(dsc, nrows, aix, av, lane, c, v);
+    else if (G == 8)
+      load_rows<8>(dsc, nrows, aix, av, lane, c, v);
+    else
+      load_rows<16>(dsc, nrows, aix, av, lane, c, v);
+  };
+
+  // ---- prologue: batch 0 descriptors + nonzeros, batch 1 descriptors,
+  // batch 2 plan words
+  uint32_t w0 = plan_word(beg);
+  int64_t rs0;
+  int len0;
+  row_desc(beg, w0, rs0, len0);
+  uint32_t w1 = plan_word(beg + R);
+  int64_t rs1;
+  int len1;
+  row_desc(beg + R, w1, rs1, len1);
+  uint32_t w2 = plan_word(beg + 2 * (int64_t)R);
+  int slot = 0;
+  IX c0[16], c1[16];
+  TV v0[16], v1[16];
+  int g0 = publish(slot, beg, rs0, len0, w0);
+  __syncwarp();
+  load_sw(g0, descs + slot * 32, (int)((end - beg) < R ? (end - beg) : R), c0, v0);
 
   for (int64_t k0 = beg; k0 < end; k0 += R) {
     const int nrows = (int)((end - k0) < R ? (end - k0) : R);
-    __syncwarp();
-    if (lane < nrows) desc[lane] = make_int4((int)(uint32_t)rs_cur, (int)(rs_cur >> 32), len_cur, (int)(w_cur >> 31));
-    const int lmax = __reduce_max_sync(0xffffffffu, lane < nrows ? len_cur : 0);
-    // prefetch: descriptors of the next batch, plan words of the one after
-    int64_t rs_n = 0;
-    int len_n = 0;
-    const int64_t k1 = k0 + R, k2 = k0 + 2 * (int64_t)R;
-    if (lane < R && k1 + lane < end) {
-      const int64_t row = w_nxt & 0x7fffffffu;
-      rs_n = (int64_t)aip[row];
-      len_n = (int)((int64_t)aip[row + 1] - rs_n);
+    const int4 *dcur = descs + slot * 32;
+    const int64_t k1 = k0 + R, k2 = k0 + 2 * (int64_t)R, k3 = k0 + 3 * (int64_t)R;
+    // ---- batch b+1: descriptors published, nonzeros in flight
+    int g1 = 4;
+    if (k1 < end) {
+      g1 = publish(slot ^ 1, k1, rs1, len1, w1);
+      __syncwarp();
+      load_sw(g1, descs + (slot ^ 1) * 32, (int)((end - k1) < R ? (end - k1) : R), c1, v1);
     }
-    const uint32_t w_n2 = (lane < R && k2 + lane < end) ? __ldg(prow + k2 + lane) : 0u;
-    __syncwarp();
-    // ---- gather + scatter into the tile
-    IX cc[16];
-    int gsel;
-    if (lmax <= 4) {
-      gsel = 4;
-      scatter_rows<4>(desc, nrows, aix, av, tile, dp, lane, cc);
-    } else if (lmax <= 8) {
-      gsel = 8;
-      scatter_rows<8>(desc, nrows, aix, av, tile, dp, lane, cc);
-    } else {
-      gsel = 16;
-      scatter_rows<16>(desc, nrows, aix, av, tile, dp, lane, cc);
-    }
-    uint32_t longm = __ballot_sync(0xffffffffu, lane < nrows && len_cur > gsel);
+    // ---- batch b+2 descriptors, batch b+3 plan words
+    int64_t rs2;
+    int len2;
+    row_desc(k2, w2, rs2, len2);
+    const uint32_t w3 = plan_word(k3);
+    // ---- scatter batch b
+    if (g0 == 4)
+      store_rows<4>(dcur, tile, dp, lane, c0, v0);
+    else if (g0 == 8)
+      store_rows<8>(dcur, tile, dp, lane, c0, v0);
+    else
+      store_rows<16>(dcur, tile, dp, lane, c0, v0);
+    uint32_t longm = __ballot_sync(0xffffffffu, lane < nrows && len0 > g0);
     const uint32_t had_long = longm;
     while (longm) {  // rows longer than G: whole warp per row
       const int r = __ffs(longm) - 1;
       longm &= longm - 1;
-      const int4 ds = desc[r];
+      const int4 ds = dcur[r];
       const int64_t rs = (int64_t)(uint32_t)ds.x | ((int64_t)ds.y << 32);
-      for (int q = gsel + lane; q < ds.z; q += 32) {
+      for (int q = g0 + lane; q < ds.z; q += 32) {
         const TV v = __ldg(av + rs + q);
         tile[r * dp + (int)__ldg(aix + rs + q)] = ds.w ? -v : v;
       }
     }
     __syncwarp();
-    // ---- accumulate the batch in row order
+    // ---- accumulate batch b in row order
     for (int r = 0; r < nrows; ++r) {
 #pragma unroll
       for (int k = 0; k < kChunks; ++k) {
@@ -157,20 +200,29 @@ __global__ void __launch_bounds__(kTileWarps * 32, 6) csr_tile_kernel(
     }
     __syncwarp();
     // ---- re-zero exactly what was written
-    if (gsel == 4)
-      unscatter_rows<4>(desc, nrows, tile, dp, lane, cc);
-    else if (gsel == 8)
-      unscatter_rows<8>(desc, nrows, tile, dp, lane, cc);
+    if (g0 == 4)
+      unscatter_rows<4>(tile, dp, lane, c0);
+    else if (g0 == 8)
+      unscatter_rows<8>(tile, dp, lane, c0);
     else
-      unscatter_rows<16>(desc, nrows, tile, dp, lane, cc);
+      unscatter_rows<16>(tile, dp, lane, c0);
     for (uint32_t m = had_long; m; m &= m - 1) {
       const int r = __ffs(m) - 1;
       for (int c = lane; c < dp; c += 32) tile[r * dp + c] = (TV)0;
     }
-    w_cur = w_nxt;
-    rs_cur = rs_n;
-    len_cur = len_n;
-    w_nxt = w_n2;
+    // ---- rotate the pipeline
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      c0[i] = c1[i];
+      v0[i] = v1[i];
+    }
+    g0 = g1;
+    len0 = len1;
+    rs1 = rs2;
+    len1 = len2;
+    w1 = w2;
+    w2 = w3;
+    slot ^= 1;
   }
   TOut *o = sa + bucket * ldsa;
 #pragma unroll

@@ -33,7 +33,11 @@ __global__ void __launch_bounds__(256) csr_atomic_kernel(const int64_t *__restri
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t k = warp; k < n; k += nwarps) {
+  // plan positions of buckets [0, t) of the (possibly offset) indptr: a
+  // bucket range [b0, b1) of the operator is indptr + b0, t = b1 - b0
+  const int64_t k_end = __ldg(pindptr + t);
+  (void)n;
+  for (int64_t k = __ldg(pindptr) + warp; k < k_end; k += nwarps) {
     // bucket of plan position k: last b with indptr[b] <= k (warp-uniform)
     int64_t lo = 0, hi = (int64_t)t;
     while (hi - lo > 1) {

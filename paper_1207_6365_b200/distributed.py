@@ -89,3 +89,66 @@ class ShardedSparseEmbedding:
 
     def descriptor(self) -> dict:
         return {"family": self.family, "n": self.input_dim, "t": self.output_dim, "seed": self.seed}
+
+
+class BucketShardedSparseEmbedding:
+    """Bucket-ownership sharding ("when row sharding is wrong"):
+    every rank holds the whole operator and the whole input, rank g owns the
+    contiguous bucket range [b_g, b_{g+1}) and computes only those SA rows,
+    reading only the rows of A hashed there (the plan's bucket-range slice).
+    There is no collective on the data path: SA stays row-block distributed
+    (``gather()`` assembles it when a caller needs the full matrix).  This is
+    the multi-GPU layout for config 5, whose m x d partial (419 MB) would
+    dwarf each GPU's share of the input under row sharding.  Within a bucket
+    the rows are still summed in ascending order, so every rank's block is
+    bit-identical to the same rows of the single-GPU (and reference) SA.
+
+    ``block_fn(a, out_dtype, (b0, b1)) -> (b1 - b0) x d`` is injectable so the
+    partition and the gather run on CPU with gloo in tests."""
+
+    family = "sparse"
+
+    def __init__(self, n: int, t: int, seed: int, group=None, device=None, block_fn=None):
+        self.input_dim, self.output_dim, self.seed = int(n), int(t), int(seed)
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.bucket_begin, self.bucket_end = shard_rows(self.output_dim, self.world, self.rank)
+        self.local = None
+        if block_fn is None:
+            from .sketch import SparseEmbedding
+
+            self.local = SparseEmbedding(n, t, seed, device=device)
+            block_fn = self._gpu_block
+        self.block_fn = block_fn
+
+    def _gpu_block(self, a, out_dtype, buckets, deterministic=True):
+        b0, b1 = buckets
+        op = self.local
+        if isinstance(a, torch.Tensor) and a.layout == torch.sparse_csr:
+            ip, ix, vv = (x.to(op.device) for x in (a.crow_indices(), a.col_indices(), a.values()))
+            out = op._apply_csr_device(ip, ix, vv, a.shape[1], out_dtype, canonical=True,
+                                       deterministic=deterministic, buckets=buckets)
+        else:
+            x = a.to(op.device)
+            out = op._apply_dense_device(x, out_dtype, check_finite=True, buckets=buckets)
+        return out[b0:b1]
+
+    def apply(self, a, out_dtype=torch.float64, **kw):
+        """This rank's SA rows [bucket_begin, bucket_end) from the full input."""
+        if a.shape[0] != self.input_dim:
+            raise ValueError(f"operator expects {self.input_dim} rows, got {a.shape[0]}")
+        return self.block_fn(a, out_dtype, (self.bucket_begin, self.bucket_end), **kw)
+
+    def gather(self, block):
+        """All ranks' blocks -> the full t x d SA on every rank (all-gather)."""
+        rows = [b1 - b0 for b0, b1 in (shard_rows(self.output_dim, self.world, r) for r in range(self.world))]
+        mx = max(rows)  # equal-size exchange (blocks differ by at most one row)
+        pad = torch.zeros((mx,) + tuple(block.shape[1:]), dtype=block.dtype, device=block.device)
+        pad[: block.shape[0]] = block
+        parts = [torch.empty_like(pad) for _ in rows]
+        dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([p[:r] for p, r in zip(parts, rows)], 0)
+
+    def descriptor(self) -> dict:
+        return {"family": self.family, "n": self.input_dim, "t": self.output_dim, "seed": self.seed}

@@ -416,26 +416,36 @@ class SparseEmbedding(SketchOperator):
     _CSR_SMEM_MAX_D = (200 * 1024 - 3328) // 8
 
     def _apply_csr_device(self, indptr, indices, vals, d: int, out_dtype, canonical: bool, out=None,
-                          shift=None, deterministic: bool = True):
+                          shift=None, deterministic: bool = True, buckets=None):
+        """K4 on device CSR arrays.  ``buckets=(b0, b1)`` computes only SA rows
+        [b0, b1) (bucket-ownership sharding); the returned tensor is the full
+        t x d ``out`` with those rows written."""
         if vals.dtype not in _TORCH_TO_SKT:
             vals = vals.to(torch.float64)
         if (deterministic and out_dtype == torch.float32 and d > self._CSR_SMEM_MAX_D and canonical
                 and out is None):
             # the wide deterministic kernel accumulates in the fp64 output row
-            return self._apply_csr_device(indptr, indices, vals, d, torch.float64, canonical).to(torch.float32)
+            return self._apply_csr_device(indptr, indices, vals, d, torch.float64, canonical,
+                                          buckets=buckets).to(torch.float32)
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
+        b0, b1 = (0, self.output_dim) if buckets is None else (int(buckets[0]), int(buckets[1]))
+        if not (0 <= b0 < b1 <= self.output_dim):
+            raise ValueError(f"bad bucket range {buckets!r}")
         if shift is None:
             shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
+        if b0 % (1 << shift):
+            shift = 0  # a grouped plan serves ranges starting on a group boundary
         gptr, grows, gblo = self.grouped_plan(shift)
         flags = (_lib.SKT_CSR_CANONICAL if canonical else 0) | (0 if deterministic else _lib.SKT_CSR_FAST)
         with torch.cuda.device(self.device):
             check(
                 _lib.lib().skt_apply_csr(
-                    _ptr(gptr), _ptr(grows), _ptr(gblo), shift, self.output_dim,
+                    _ptr(gptr) + 8 * (b0 >> shift), _ptr(grows), _ptr(gblo), shift, b1 - b0,
                     self.row_end - self.row_begin, _ptr(indptr), _ITYPE[indptr.dtype], _ptr(indices),
                     _ITYPE[indices.dtype], _ptr(vals), _TORCH_TO_SKT[vals.dtype], vals.numel(), d,
-                    _ptr(out), _TORCH_TO_SKT[out.dtype], max(d, 1), flags, _stream_ptr(self.device),
+                    _ptr(out) + b0 * out.stride(0) * out.element_size(), _TORCH_TO_SKT[out.dtype], max(d, 1),
+                    flags, _stream_ptr(self.device),
                 )
             )
         return out

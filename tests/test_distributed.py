@@ -89,3 +89,56 @@ def test_two_rank_gloo_allreduce_matches_reference(kind):
     rel, r0, r1 = q.get(timeout=10)
     assert (r0, r1) == (0, 2500)
     assert rel <= 1e-12
+
+
+def _bucket_worker(rank, world, port, n, t, d, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        import scipy.sparse as sp
+
+        from paper_1207_6365_b200.distributed import BucketShardedSparseEmbedding
+
+        rng = np.random.default_rng(321)
+        h, s = O.hash_signs(n, t, seed)
+        a = sp.csr_array(sp.random_array((n, d), density=0.05, rng=rng, format="csr"))
+
+        def block(a_full, out_dtype, buckets):
+            # the GPU kernel's role: SA rows [b0, b1) only, from the rows hashed there
+            b0, b1 = buckets
+            mine = np.flatnonzero((h >= b0) & (h < b1))
+            part = O.apply_csr(h[mine] - b0, s[mine], b1 - b0, sp.csr_array(a_full)[mine])
+            return torch.from_numpy(part).to(out_dtype)
+
+        op = BucketShardedSparseEmbedding(n, t, seed, block_fn=block)
+        blk = op.apply(a)
+        full = op.gather(blk).numpy()
+        ref = O.apply(h, s, t, a)
+        if rank == 0:
+            q.put((bool(np.array_equal(full, ref)), op.bucket_begin, op.bucket_end, blk.shape[0]))
+        with pytest.raises(ValueError):
+            op.apply(a[:10])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_bucket_ownership_matches_reference():
+    """Bucket-ownership sharding (config 5's multi-GPU layout): each rank's SA
+    block covers its bucket range, computed from the rows hashed there; the
+    all-gathered SA equals the single-process reference bit for bit (no
+    reassociation: every bucket is summed on one rank, in ascending row order)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n, t, d, seed = 4_001, 101, 300, 5
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, n, t, d, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    same, b0, b1, rows = q.get(timeout=10)
+    assert (b0, b1, rows) == (0, 50, 50)
+    assert same
