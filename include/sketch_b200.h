@@ -158,6 +158,23 @@ skt_status skt_lev_rownorms_dense(int64_t n, int64_t d, const void *a, skt_dtype
                                   int64_t lda, const double *probe, int64_t k, void *scores,
                                   skt_dtype score_dtype, int32_t *nonfinite_flag, void *stream);
 
+/* ---- residual pass on the original data --------------------------------- */
+/* Replaces regress.py:81-82 (_residual_fro: ||a @ x - b||_F, the step after
+ * every sketch-and-solve): *out_sq (device fp64) = sum_ij ((A X)_ij - B_ij)^2,
+ * fused with the GEMV / SpMV so A is read once.  X is d x k fp64 row-major,
+ * B is n x k (ldb) f32 or f64; A dense (lda) or CSR.  The workspace holds one
+ * fp64 partial per block (skt_residual_workspace); the fixed-order block
+ * reduction makes the result deterministic. */
+skt_status skt_residual_workspace(size_t *bytes);
+skt_status skt_residual_dense(int64_t n, int64_t d, const void *a, skt_dtype a_dtype, int64_t lda,
+                              const double *x, int64_t k, const void *b, skt_dtype b_dtype,
+                              int64_t ldb, double *out_sq, void *ws, size_t ws_bytes, void *stream);
+skt_status skt_residual_csr(int64_t n, int64_t d, const void *a_indptr, skt_itype indptr_type,
+                            const void *a_indices, skt_itype index_type, const void *a_vals,
+                            skt_dtype val_dtype, const double *x, int64_t k, const void *b,
+                            skt_dtype b_dtype, int64_t ldb, double *out_sq, void *ws,
+                            size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

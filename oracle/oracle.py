@@ -223,3 +223,9 @@ def np_lev_rownorms(a, probe: np.ndarray) -> np.ndarray:
     """leverage.py:90-91."""
     rows = np.asarray(a @ probe)
     return np.einsum("ij,ij->i", rows, rows)
+
+
+def residual_fro(a, x, b) -> float:
+    """||a @ x - b||_F exactly as regress.py:79-80 (_residual_fro) computes it:
+    the reference's own numpy / scipy product, then the Frobenius norm."""
+    return float(np.linalg.norm(np.asarray(a @ x) - b, "fro"))

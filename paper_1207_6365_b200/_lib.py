@@ -42,6 +42,9 @@ EXPORTS = (
     "skt_apply_right_csr",
     "skt_lev_rownorms_csr",
     "skt_lev_rownorms_dense",
+    "skt_residual_workspace",
+    "skt_residual_dense",
+    "skt_residual_csr",
 )
 
 
@@ -106,6 +109,9 @@ def lib() -> ctypes.CDLL:
         "skt_apply_right_csr": ([P, P, u64, i64, i64, P, i32, P, i32, P, i32, P, i32, i64, P], i32),
         "skt_lev_rownorms_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, P], i32),
         "skt_lev_rownorms_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, P, P], i32),
+        "skt_residual_workspace": ([ctypes.POINTER(sz)], i32),
+        "skt_residual_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, i64, P, P, sz, P], i32),
+        "skt_residual_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, i64, P, P, sz, P], i32),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

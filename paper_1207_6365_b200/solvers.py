@@ -94,23 +94,54 @@ class RegressionSolution:
     coreset: object = None
 
 
+def residual_fro(a, x, b, device=None) -> float:
+    """||A x - b||_F (regress.py:81-82) in one fused pass over A on the GPU
+    (skt_residual_dense / skt_residual_csr).  ``a``: numpy / scipy CSR / torch;
+    ``x``: d x k (or d); ``b``: n x k (or n)."""
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    L = _lib.lib()
+    n, d = a.shape[0], a.shape[1]
+    xt = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64) if not isinstance(x, torch.Tensor) else x)
+    xt = xt.to(device=device, dtype=torch.float64).reshape(d, -1).contiguous()
+    k = xt.shape[1]
+    bt = torch.as_tensor(np.ascontiguousarray(b) if not isinstance(b, torch.Tensor) else b).to(device)
+    if bt.dtype not in _TORCH_TO_SKT:
+        bt = bt.to(torch.float64)
+    bt = bt.reshape(n, -1).contiguous()
+    if bt.shape[1] != k:
+        raise ValueError(f"x has {k} columns, b has {bt.shape[1]}")
+    ws_bytes = ctypes.c_size_t()
+    check(L.skt_residual_workspace(ctypes.byref(ws_bytes)))
+    ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=device)
+    out = torch.empty(1, dtype=torch.float64, device=device)
+    with torch.cuda.device(device):
+        stream = _stream_ptr(device)
+        if sp.issparse(a) or (isinstance(a, torch.Tensor) and a.layout == torch.sparse_csr):
+            if isinstance(a, torch.Tensor):
+                ip, ix, vv = (t.to(device) for t in (a.crow_indices(), a.col_indices(), a.values()))
+            else:
+                m = sp.csr_array(a)
+                ip, ix, vv = (torch.from_numpy(np.ascontiguousarray(t)).to(device)
+                              for t in (m.indptr, m.indices, m.data))
+            if vv.dtype not in _TORCH_TO_SKT:
+                vv = vv.to(torch.float64)
+            check(L.skt_residual_csr(n, d, _ptr(ip), _ITYPE[ip.dtype], _ptr(ix), _ITYPE[ix.dtype], _ptr(vv),
+                                     _TORCH_TO_SKT[vv.dtype], _ptr(xt), k, _ptr(bt), _TORCH_TO_SKT[bt.dtype],
+                                     k, _ptr(out), _ptr(ws), ws_bytes.value, stream))
+        else:
+            at = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+            at = at.to(device)
+            if at.dtype not in _TORCH_TO_SKT:
+                at = at.to(torch.float64)
+            at = at.reshape(n, -1).contiguous()
+            check(L.skt_residual_dense(n, d, _ptr(at), _TORCH_TO_SKT[at.dtype], max(d, 1), _ptr(xt), k, _ptr(bt),
+                                       _TORCH_TO_SKT[bt.dtype], k, _ptr(out), _ptr(ws), ws_bytes.value, stream))
+    return math.sqrt(float(out.item()))
+
+
 def _residual_fro_gpu(a, x: np.ndarray, b: np.ndarray, device) -> float:
-    """||A x - b||_F on the device (regress.py:81-82)."""
-    xt = torch.from_numpy(np.ascontiguousarray(x)).to(device)
-    bt = torch.from_numpy(np.ascontiguousarray(b)).to(device)
-    if sp.issparse(a):
-        m = sp.csr_array(a)
-        at = torch.sparse_csr_tensor(
-            torch.from_numpy(m.indptr.astype(np.int64)).to(device),
-            torch.from_numpy(m.indices.astype(np.int64)).to(device),
-            torch.from_numpy(m.data.astype(np.float64)).to(device),
-            size=m.shape,
-        )
-        r = at @ xt - bt
-    else:
-        at = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
-        r = at @ xt - bt
-    return float(torch.linalg.norm(r).item())
+    return residual_fro(a, x, b, device)
 
 
 def sketch_solve_ls(a, b, eps: float, seed: int = 0, operator=None) -> RegressionSolution:
