@@ -120,32 +120,16 @@ def peak_hbm():
         return 6650.0, "fallback"
 
 
-def gather_ceiling_ms(rows: int, seg_bytes):
-    """Time to gather `rows` x (one segment of each size in seg_bytes) at random
-    offsets, at the segment rates measured by tools/gather_bench.cu (log-linear
-    interpolation; segments below 16 B cost one 16 B request)."""
-    import math
-
+def gather_ceiling_ms(cfg_name: str):
+    """The config's CSR access pattern run without arithmetic (random row
+    order, indptr pair + index / value segments per row; tools/gather_bench.cu,
+    profiles/r01_gather_ceiling.json), or None."""
     p = os.path.join(ROOT, "profiles", "r01_gather_ceiling.json")
     try:
         with open(p) as f:
-            tab = {int(k): float(v) for k, v in json.load(f)["unaligned"].items()}
+            return float(json.load(f)["csr_pattern_ms"][cfg_name])
     except Exception:
         return None
-    sizes = sorted(tab)
-    rate = {s: tab[s] * 1e9 / s for s in sizes}  # segments per second
-    t = 0.0
-    for b in seg_bytes:
-        s = min(max(b, sizes[0]), sizes[-1])
-        lo = max(x for x in sizes if x <= s)
-        hi = min(x for x in sizes if x >= s)
-        if lo == hi:
-            r = rate[lo]
-        else:
-            f = (math.log2(s) - math.log2(lo)) / (math.log2(hi) - math.log2(lo))
-            r = math.exp((1 - f) * math.log(rate[lo]) + f * math.log(rate[hi]))
-        t += rows / r
-    return 1e3 * t
 
 
 def traffic_for(cfg_name: str):
@@ -520,18 +504,15 @@ def our_arm(args, cfg):
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
                 "kernel_ms": round(kern_ms, 4), "alg_bytes_per_launch": alg_bytes,
                 "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}
-    if cfg["kind"] == "csr" and lev is None and not cfg.get("fast"):
+    gc = gather_ceiling_ms(args.config) if (cfg["kind"] == "csr" and lev is None and world == 1) else None
+    if gc is not None:
         # CSR S.A reads every row's (indptr pair, index segment, value segment)
-        # in bucket order = random rows: its ceiling is the random-segment
-        # gather rate measured by tools/gather_bench.cu, not streaming HBM
-        rows_local = r1 - r0
-        per_row = nnz_local / max(rows_local, 1)
-        gc = gather_ceiling_ms(rows_local, [8.0, per_row * ix.element_size(), per_row * vv.element_size()])
-        if gc is not None:
-            roofline["gather_ceiling"] = {
-                "ms": round(gc, 4), "frac": round(gc / kern_ms, 4),
-                "model": "per row: 8 B indptr pair + index segment + value segment at random offsets, each at "
-                         "the measured random-segment rate for its size (profiles/r01_gather_ceiling.json)"}
+        # in bucket order = random rows, which B200 serves at a request rate
+        # well below streaming HBM: the kernel's ceiling is that access pattern
+        roofline["gather_ceiling"] = {
+            "ms": gc, "frac": round(gc / kern_ms, 4),
+            "source": "the same access pattern without arithmetic, L2 flushed (tools/gather_bench.cu, "
+                      "profiles/r01_gather_ceiling.json)"}
 
     # ---- end to end through the public API, host buffers
     e2e = None

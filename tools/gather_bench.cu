@@ -55,12 +55,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const float *__restrict__ p
 
 // CSR S.A's access pattern without its arithmetic: rows visited in a random
 // order (a permutation, like the bucket-ordered plan), per row the indptr
-// pair, then the row's index and value segments (16 lanes per row, two rows
+// pair, then the row's index and value segments (G lanes per row, 32/G rows
 // per instruction, the batch's 32 rows' loads all issued before use, the next
 // batch's indptr pairs in flight) -- the ceiling for configs 2 / 4.
+template <int G, typename TV>
 __global__ void __launch_bounds__(128) csr_gather_kernel(const uint32_t *__restrict__ perm, int64_t n,
                                                          const int *__restrict__ ip, const int *__restrict__ ix,
-                                                         const float *__restrict__ v, float *out) {
+                                                         const TV *__restrict__ v, float *out) {
+  constexpr int S = 32 / G;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -80,41 +82,42 @@ __global__ void __launch_bounds__(128) csr_gather_kernel(const uint32_t *__restr
       rs_n = ip[r];
       len_n = ip[r + 1] - rs_n;
     }
-    int c[16];
-    float x[16];
+    int c[G];
+    TV x[G];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int row = 2 * i + (lane >> 4);
+    for (int i = 0; i < G; ++i) {
+      const int row = S * i + lane / G;
       const int s = __shfl_sync(0xffffffffu, rs, row), l = __shfl_sync(0xffffffffu, len, row);
       c[i] = 0;
-      x[i] = 0.f;
-      if ((lane & 15) < l) {
-        c[i] = __ldg(ix + s + (lane & 15));
-        x[i] = __ldg(v + s + (lane & 15));
+      x[i] = (TV)0;
+      if ((lane % G) < l) {
+        c[i] = __ldg(ix + s + (lane % G));
+        x[i] = __ldg(v + s + (lane % G));
       }
     }
-    const uint32_t longm = __ballot_sync(0xffffffffu, len > 16);
+    const uint32_t longm = __ballot_sync(0xffffffffu, len > G);
     for (uint32_t m = longm; m; m &= m - 1) {
       const int row = __ffs(m) - 1;
       const int s = __shfl_sync(0xffffffffu, rs, row), l = __shfl_sync(0xffffffffu, len, row);
-      for (int q = 16 + lane; q < l; q += 32) acc += (float)__ldg(ix + s + q) + __ldg(v + s + q);
+      for (int q = G + lane; q < l; q += 32) acc += (float)__ldg(ix + s + q) + (float)__ldg(v + s + q);
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc += (float)c[i] + x[i];
+    for (int i = 0; i < G; ++i) acc += (float)c[i] + (float)x[i];
     rs = rs_n;
     len = len_n;
   }
   if (acc == 12345.678f) out[0] = acc;
 }
 
-void run_csr() {
-  const int64_t n = 4194304;
+// name, rows, nonzeros per row (1% of rows dense_len when dense_len > 0), value type
+template <int G, typename TV>
+void run_csr(const char *name, int64_t n, int per, int dense_len) {
   std::vector<int> ip(n + 1);
   ip[0] = 0;
   uint64_t st = 1;
   for (int64_t r = 0; r < n; ++r) {
     st = st * 6364136223846793005ULL + 1442695040888963407ULL;
-    ip[r + 1] = ip[r] + ((st >> 33) % 100 == 0 ? 64 : 16);
+    ip[r + 1] = ip[r] + ((dense_len > 0 && (st >> 33) % 100 == 0) ? dense_len : per);
   }
   const int64_t nnz = ip[n];
   std::vector<uint32_t> perm(n);
@@ -125,16 +128,20 @@ void run_csr() {
     std::swap(perm[i], perm[j]);
   }
   int *dip, *dix;
-  float *dv, *out;
+  TV *dv;
+  float *out;
   uint32_t *dperm;
   cudaMalloc(&dip, (n + 1) * 4);
   cudaMalloc(&dix, nnz * 4);
-  cudaMalloc(&dv, nnz * 4);
+  cudaMalloc(&dv, nnz * sizeof(TV));
   cudaMalloc(&dperm, n * 4);
   cudaMalloc(&out, 4);
   cudaMemset(dix, 0, nnz * 4);
-  cudaMemset(dv, 0, nnz * 4);
+  cudaMemset(dv, 0, nnz * sizeof(TV));
   cudaMemcpy(dip, ip.data(), (n + 1) * 4, cudaMemcpyHostToDevice);
+  // L2 flush buffer for inputs that fit in L2
+  char *flush;
+  cudaMalloc(&flush, 512 << 20);
   for (int ordered = 0; ordered < 2; ++ordered) {
     cudaMemcpy(dperm, perm.data(), n * 4, cudaMemcpyHostToDevice);
     if (ordered) {
@@ -146,20 +153,31 @@ void run_csr() {
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
-      csr_gather_kernel<<<blocks, 128>>>(dperm, n, dip, dix, dv, out);
-      cudaEventRecord(a);
-      for (int i = 0; i < 5; ++i) csr_gather_kernel<<<blocks, 128>>>(dperm, n, dip, dix, dv, out);
-      cudaEventRecord(b);
-      cudaEventSynchronize(b);
-      float ms;
-      cudaEventElapsedTime(&ms, a, b);
-      ms /= 5;
-      const double alg = nnz * 8.0 + (n + 1) * 4.0;
-      printf("csr gather (config-4 shape, %s rows, %d CTAs): %.4f ms, %.0f GB/s algorithmic (%s)\n",
+      csr_gather_kernel<G, TV><<<blocks, 128>>>(dperm, n, dip, dix, dv, out);
+      float total = 0.f;
+      for (int i = 0; i < 5; ++i) {
+        cudaMemsetAsync(flush, i, 512 << 20);
+        cudaEventRecord(a);
+        csr_gather_kernel<G, TV><<<blocks, 128>>>(dperm, n, dip, dix, dv, out);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        total += ms;
+      }
+      const float ms = total / 5;
+      const double alg = nnz * (4.0 + sizeof(TV)) + (n + 1) * 4.0;
+      printf("csr gather (%s shape, %s rows, %d CTAs, L2 flushed): %.4f ms, %.0f GB/s algorithmic (%s)\n", name,
              ordered ? "sequential" : "random", blocks, ms, alg / (ms * 1e-3) / 1e9,
              cudaGetErrorString(cudaGetLastError()));
     }
   }
+  cudaFree(dip);
+  cudaFree(dix);
+  cudaFree(dv);
+  cudaFree(dperm);
+  cudaFree(out);
+  cudaFree(flush);
 }
 
 template <int kSeg, int kU>
@@ -185,7 +203,8 @@ void run(const float *p, int64_t nfloats, float *out, int align) {
 }
 
 int main() {
-  run_csr();
+  run_csr<16, float>("config-4", 4194304, 16, 64);
+  run_csr<8, double>("config-2", 1000000, 5, 0);
   const int64_t nfloats = (int64_t)2 << 30;  // 8 GB
   float *p, *out;
   cudaMalloc(&p, nfloats * 4);
