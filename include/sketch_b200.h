@@ -175,6 +175,19 @@ skt_status skt_residual_csr(int64_t n, int64_t d, const void *a_indptr, skt_ityp
                             skt_dtype b_dtype, int64_t ldb, double *out_sq, void *ws,
                             size_t ws_bytes, void *stream);
 
+/* ---- SRHT of a tall fp64 matrix ---------------------------------------- */
+/* Replaces SrhtOperator.apply (sketch.py:284-291) on device data: rows of A
+ * (n x d, lda) zero-padded to n_pad = 2^ceil(log2 n), multiplied by sign[i]
+ * (n_pad entries, +-1.0), unnormalised Walsh-Hadamard transform along the
+ * rows (_fwht, sketch.py:241-252 -- the same butterflies in the same stage
+ * order, so bit-identical), then out[r, :] = scale * H[rows[r], :] for the t
+ * sampled rows.  The workspace holds the n_pad x d transform
+ * (skt_srht_workspace). */
+skt_status skt_srht_workspace(int64_t n, int64_t d, size_t *bytes);
+skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, const double *sign,
+                          const int64_t *rows, int64_t t, double scale, double *out, int64_t ldo,
+                          void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -229,3 +229,30 @@ def residual_fro(a, x, b) -> float:
     """||a @ x - b||_F exactly as regress.py:79-80 (_residual_fro) computes it:
     the reference's own numpy / scipy product, then the Frobenius norm."""
     return float(np.linalg.norm(np.asarray(a @ x) - b, "fro"))
+
+
+def srht_apply(a: np.ndarray, t: int, seed: int) -> np.ndarray:
+    """SrhtOperator(n, t, seed).apply(a) restated (sketch.py:241-252 _fwht,
+    sketch.py:266-291 __init__ / apply): zero-pad to n_pad = 2^ceil(log2 n),
+    sign flip from stream (2, 0), unnormalised Walsh-Hadamard along rows, t rows
+    sampled from stream (2, 1), scaled by sqrt(n_pad/t)/sqrt(n_pad)."""
+    import math
+
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    n = a.shape[0]
+    n_pad = 1 << (n - 1).bit_length()
+    rng = lambda k: np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, k)))  # noqa: E731
+    sign = rng(0).choice(np.array([-1.0, 1.0]), size=n_pad)
+    rows = rng(1).integers(0, n_pad, size=t)
+    scale = math.sqrt(n_pad / t) / math.sqrt(n_pad)
+    out = np.zeros((n_pad, a.shape[1]))
+    out[:n] = a
+    out *= sign[:, None]
+    h = 1
+    while h < n_pad:
+        out = out.reshape(n_pad // (2 * h), 2, h, -1)
+        out = np.stack((out[:, 0] + out[:, 1], out[:, 0] - out[:, 1]), axis=1).reshape(n_pad, -1)
+        h *= 2
+    return scale * out[rows]

@@ -278,24 +278,45 @@ def leverage_scores_sketched(a, m: int, k: int, seed: int, rep: int = 0) -> Leve
     return LeverageRun(scores, rank, sa, probe)
 
 
-def _srht_apply(sa: np.ndarray, t: int, seed: int) -> np.ndarray:
-    """SrhtOperator(n, t, seed).apply (sketch.py:241-302) restated on the host:
-    a thin step on the small sketch (t1 x d) -- not part of the GPU hot path."""
-    n = sa.shape[0]
+def srht_apply(a, t: int, seed: int, device=None):
+    """SrhtOperator(n, t, seed).apply(a) (sketch.py:255-291) on the GPU
+    (skt_srht_apply: sign flip + padding, the reference's _fwht butterflies
+    stage by stage, sampling + scaling), bit-identical to the reference.  The
+    sign vector and the sampled rows are the reference's streams (2, 0) and
+    (2, 1) of SeedSequence(seed) (numpy, host; n_pad + t draws).  ``a``: numpy
+    or torch (n x d or n); returns the same kind (torch on ``a``'s device)."""
+    if device is None:
+        device = a.device if isinstance(a, torch.Tensor) and a.is_cuda else torch.device(
+            "cuda", torch.cuda.current_device())
+    host = not isinstance(a, torch.Tensor)
+    x = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64) if host else a)
+    x = x.to(device=device, dtype=torch.float64)
+    one_d = x.dim() == 1
+    x = x.reshape(x.shape[0], -1).contiguous()
+    n, d = x.shape
+    if n < 1 or t < 1:
+        raise ValueError("n and t must be >= 1")
     n_pad = 1 << (n - 1).bit_length()
-    sign = np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, 0))).choice(
-        np.array([-1.0, 1.0]), size=n_pad)
-    rows = np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, 1))).integers(0, n_pad, size=t)
+    if t > n_pad:
+        raise ValueError(f"t={t} exceeds padded dimension {n_pad}")
+
+    def rng(k):
+        return np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, k)))
+
+    sign = torch.from_numpy(rng(0).choice(np.array([-1.0, 1.0]), size=n_pad)).to(device)
+    rows = torch.from_numpy(rng(1).integers(0, n_pad, size=t).astype(np.int64)).to(device)
     scale = math.sqrt(n_pad / t) / math.sqrt(n_pad)
-    out = np.zeros((n_pad, sa.shape[1]))
-    out[:n] = sa
-    out *= sign[:, None]
-    h = 1
-    while h < n_pad:  # _fwht (sketch.py:241-252)
-        out = out.reshape(n_pad // (2 * h), 2, h, -1)
-        out = np.stack((out[:, 0] + out[:, 1], out[:, 0] - out[:, 1]), axis=1).reshape(n_pad, -1)
-        h *= 2
-    return scale * out[rows]
+    out = torch.empty((t, d), dtype=torch.float64, device=device)
+    L = _lib.lib()
+    wsb = ctypes.c_size_t()
+    check(L.skt_srht_workspace(n, d, ctypes.byref(wsb)))
+    ws = torch.empty(max(wsb.value, 8), dtype=torch.uint8, device=device)
+    with torch.cuda.device(device):
+        check(L.skt_srht_apply(_ptr(x), n, d, max(d, 1), _ptr(sign), _ptr(rows), t, scale, _ptr(out), max(d, 1),
+                               _ptr(ws), wsb.value, _stream_ptr(device)))
+    if one_d:
+        out = out.reshape(-1)
+    return _host(out).numpy() if host else out
 
 
 @dataclass(frozen=True)
@@ -310,9 +331,10 @@ class LeverageScores:
 
 
 def approx_leverage_scores(a, eps: float, repetitions: int = 5, seed: int = 0) -> LeverageScores:
-    """leverage.py:50-97 with the sketch (K3/K4) and the fused contraction +
-    row norms (K5) on the GPU; the pivoted QR / SRHT / basis change of the
-    small sketch and the median stay on the host as in the reference."""
+    """leverage.py:50-97 with the sketch (K3/K4), the SRHT of the sketch and
+    the fused contraction + row norms (K5) on the GPU; the pivoted QR / basis
+    change of the small sketch and the median stay on the host as in the
+    reference."""
     from .sketch import check_count  # noqa: PLC0415
 
     eps = check_eps(eps)
@@ -334,7 +356,7 @@ def approx_leverage_scores(a, eps: float, repetitions: int = 5, seed: int = 0) -
             continue
         log_r = math.log(max(rank, 2))
         t_f = max(rank + 1, math.ceil(40.0 * rank * log_r * log_r))  # _srht_rows (leverage.py:105-107)
-        fsa = sa if t_f >= sa.shape[0] else _srht_apply(sa, t_f, int(sub[1]))
+        fsa = sa if t_f >= sa.shape[0] else srht_apply(sa, t_f, int(sub[1]))
         n_mat, rank2 = basis_change(fsa)
         ranks.append(rank2)
         if rank2 == 0:
@@ -359,5 +381,9 @@ __all__ = [
     "gaussian_jl_entries",
     "lev_rownorms",
     "leverage_scores_sketched",
+    "approx_leverage_scores",
+    "LeverageScores",
+    "residual_fro",
+    "srht_apply",
     "seed_words",
 ]

@@ -200,6 +200,21 @@ def configs():
         json.dump(res, f, indent=1)
 
 
+def srht_cases():
+    """SrhtOperator(n, t, seed).apply on seeded inputs (sketch.py:241-297): the
+    reference's own SRHT, for the GPU transform's bit-exact check."""
+    g = np.random.default_rng(777)
+    out, meta = {}, []
+    for k, (n, d, t, seed) in enumerate([(1, 3, 1, 0), (5, 2, 4, 1), (1000, 7, 300, 2), (4097, 33, 700, 3),
+                                          (20_000, 6, 2_000, 4)]):
+        a = g.standard_normal((n, d))
+        out[f"a{k}"] = a
+        out[f"y{k}"] = RS.SrhtOperator(n, t, seed).apply(a)
+        meta.append([n, d, t, seed])
+    out["meta"] = np.asarray(meta, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "srht_cases.npz"), **out)
+
+
 def seeds():
     rows = []
     for seed, key in [(0, ()), (1, (0, 0)), (1, (0, 1)), (5, (3,)), (2**40 + 17, (0, 0)),
@@ -216,6 +231,7 @@ def seeds():
 if __name__ == "__main__":
     assert "reference" in os.path.dirname(sketchnla.__file__), sketchnla.__file__
     seeds()
+    srht_cases()
     hash_cases()
     apply_cases()
     configs()
