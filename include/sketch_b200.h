@@ -184,8 +184,8 @@ skt_status skt_residual_csr(int64_t n, int64_t d, const void *a_indptr, skt_ityp
  * sampled rows.  The workspace holds the n_pad x d transform
  * (skt_srht_workspace). */
 skt_status skt_srht_workspace(int64_t n, int64_t d, size_t *bytes);
-skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, const double *sign,
-                          const int64_t *rows, int64_t t, double scale, double *out, int64_t ldo,
+skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, const int8_t *sign,
+                          const uint32_t *rows, int64_t t, double scale, double *out, int64_t ldo,
                           void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus

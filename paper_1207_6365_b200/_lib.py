@@ -115,7 +115,7 @@ def lib() -> ctypes.CDLL:
         "skt_residual_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, i64, P, P, sz, P], i32),
         "skt_residual_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, i64, P, P, sz, P], i32),
         "skt_srht_workspace": ([i64, i64, ctypes.POINTER(sz)], i32),
-        "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),
+        "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),  # noqa: E501
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

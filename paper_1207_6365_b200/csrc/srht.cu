@@ -23,11 +23,11 @@ constexpr int kSrhtCols = 16;   // column slice per block
 constexpr int kSrhtMaxK = 9;    // stages per pass: 512 rows x 16 cols x 8 B = 64 KB
 
 __global__ void srht_load_kernel(const double *__restrict__ a, int64_t n, int64_t d, int64_t lda,
-                                 const double *__restrict__ sign, int64_t n_pad, double *__restrict__ ws) {
+                                 const int8_t *__restrict__ sign, int64_t n_pad, double *__restrict__ ws) {
   const int64_t total = n_pad * d;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / d, c = e - i * d;
-    ws[e] = i < n ? a[i * lda + c] * sign[i] : 0.0;
+    ws[e] = i < n ? a[i * lda + c] * (double)sign[i] : 0.0;
   }
 }
 
@@ -64,12 +64,12 @@ __global__ void __launch_bounds__(kSrhtThreads) fwht_pass_kernel(double *__restr
   }
 }
 
-__global__ void srht_gather_kernel(const double *__restrict__ ws, int64_t d, const int64_t *__restrict__ rows,
+__global__ void srht_gather_kernel(const double *__restrict__ ws, int64_t d, const uint32_t *__restrict__ rows,
                                    int64_t t, double scale, double *__restrict__ out, int64_t ldo) {
   const int64_t total = t * d;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / d, c = e - r * d;
-    out[r * ldo + c] = scale * ws[rows[r] * d + c];
+    out[r * ldo + c] = scale * ws[(int64_t)rows[r] * d + c];
   }
 }
 
@@ -90,8 +90,8 @@ extern "C" skt_status skt_srht_workspace(int64_t n, int64_t d, size_t *bytes) {
   return SKT_OK;
 }
 
-extern "C" skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, const double *sign,
-                                     const int64_t *rows, int64_t t, double scale, double *out, int64_t ldo,
+extern "C" skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, const int8_t *sign,
+                                     const uint32_t *rows, int64_t t, double scale, double *out, int64_t ldo,
                                      void *ws, size_t ws_bytes, void *stream_) {
   static const char *fn = "skt_srht_apply";
   if (n < 1 || d < 0 || t < 0 || lda < d || ldo < d || (n > 0 && d > 0 && (!a || !sign)) ||

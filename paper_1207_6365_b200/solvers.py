@@ -32,6 +32,7 @@ from .sketch import (
     _stream_ptr,
     check_eps,
     default_sparse_dim,
+    pcg64_state,
     seed_words,
     sparse_embedding_or_identity,
 )
@@ -283,8 +284,8 @@ def srht_apply(a, t: int, seed: int, device=None):
     (skt_srht_apply: sign flip + padding, the reference's _fwht butterflies
     stage by stage, sampling + scaling), bit-identical to the reference.  The
     sign vector and the sampled rows are the reference's streams (2, 0) and
-    (2, 1) of SeedSequence(seed) (numpy, host; n_pad + t draws).  ``a``: numpy
-    or torch (n x d or n); returns the same kind (torch on ``a``'s device)."""
+    (2, 1) of SeedSequence(seed), drawn on the GPU by K1.  ``a``: numpy or
+    torch (n x d or n); returns the same kind (torch on ``a``'s device)."""
     if device is None:
         device = a.device if isinstance(a, torch.Tensor) and a.is_cuda else torch.device(
             "cuda", torch.cuda.current_device())
@@ -300,20 +301,27 @@ def srht_apply(a, t: int, seed: int, device=None):
     if t > n_pad:
         raise ValueError(f"t={t} exceeds padded dimension {n_pad}")
 
-    def rng(k):
-        return np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(2, k)))
-
-    sign = torch.from_numpy(rng(0).choice(np.array([-1.0, 1.0]), size=n_pad)).to(device)
-    rows = torch.from_numpy(rng(1).integers(0, n_pad, size=t).astype(np.int64)).to(device)
     scale = math.sqrt(n_pad / t) / math.sqrt(n_pad)
     out = torch.empty((t, d), dtype=torch.float64, device=device)
     L = _lib.lib()
-    wsb = ctypes.c_size_t()
-    check(L.skt_srht_workspace(n, d, ctypes.byref(wsb)))
-    ws = torch.empty(max(wsb.value, 8), dtype=torch.uint8, device=device)
     with torch.cuda.device(device):
+        stream = _stream_ptr(device)
+        # sign = stream (2, 0) .choice over n_pad, rows = stream (2, 1)
+        # .integers(0, n_pad, t): one K1 call (bucket stream (2, 1), t = n_pad)
+        hs, ss = pcg64_state(seed, (2, 1)), pcg64_state(seed, (2, 0))
+        rows = torch.empty(n_pad, dtype=torch.int32, device=device)
+        sign = torch.empty(n_pad, dtype=torch.int8, device=device)
+        kb = ctypes.c_size_t()
+        check(L.skt_hash_signs_workspace(n_pad, n_pad, ctypes.byref(kb)))
+        kws = torch.empty(max(kb.value, 8), dtype=torch.uint8, device=device)
+        check(L.skt_hash_signs(ctypes.byref(hs), ctypes.byref(ss), 0, n_pad, n_pad, _ptr(rows), _ptr(sign),
+                               _ptr(kws), kb.value, stream))
+        wsb = ctypes.c_size_t()
+        check(L.skt_srht_workspace(n, d, ctypes.byref(wsb)))
+        ws = torch.empty(max(wsb.value, 8), dtype=torch.uint8, device=device)
         check(L.skt_srht_apply(_ptr(x), n, d, max(d, 1), _ptr(sign), _ptr(rows), t, scale, _ptr(out), max(d, 1),
-                               _ptr(ws), wsb.value, _stream_ptr(device)))
+                               _ptr(ws), wsb.value, stream))
+        torch.cuda.current_stream(device).synchronize()  # workspaces freed after the stream consumed them
     if one_d:
         out = out.reshape(-1)
     return _host(out).numpy() if host else out
