@@ -256,3 +256,32 @@ def srht_apply(a: np.ndarray, t: int, seed: int) -> np.ndarray:
         out = np.stack((out[:, 0] + out[:, 1], out[:, 0] - out[:, 1]), axis=1).reshape(n_pad, -1)
         h *= 2
     return scale * out[rows]
+
+
+def gse_operator(n: int, r: int, eps: float, delta: float, seed: int):
+    """GeneralizedSparseEmbedding's hashes and matrix restated (sketch.py:69-80
+    generalized_dims, sketch.py:186-220 __init__): returns (q, k, v, t, outer,
+    inner, sign, mat) with mat the t x n scipy CSR the reference multiplies by."""
+    import math
+
+    k = max(1, math.ceil(1.0 * math.log(r / (eps * delta)) / eps))
+    v = max(1, math.ceil(1.0 / eps))
+    q = max(1, math.ceil(1.0 * r * (r + math.log(1.0 / (delta * eps))) / eps**2))
+    t = q * k * v
+    rng = lambda s: np.random.default_rng(np.random.SeedSequence(int(seed), spawn_key=(1, s)))  # noqa: E731
+    outer = rng(0).integers(0, q, size=n)
+    inner = rng(1).integers(0, v, size=(k, n))
+    sign = rng(2).choice(np.array([-1.0, 1.0]), size=(k, n))
+    rows = outer[None, :] * (k * v) + np.arange(k)[:, None] * v + inner
+    cols = np.broadcast_to(np.arange(n), (k, n))
+    mat = sp.csr_array(((sign / math.sqrt(k)).ravel(), (rows.ravel(), cols.ravel())), shape=(t, n))
+    return q, k, v, t, outer, inner, sign, mat
+
+
+def gse_apply(mat, a) -> np.ndarray:
+    """sketch.py:222-227: the reference's own product (scipy csr_matvecs /
+    csr_matmat), fp64."""
+    out = mat @ a
+    if sp.issparse(out):
+        out = out.toarray()
+    return np.asarray(out, dtype=np.float64)

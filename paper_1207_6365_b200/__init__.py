@@ -21,6 +21,7 @@ from .sketch import (
     sparse_embedding_or_identity,
     to_descriptor,
 )
+from .generalized import GeneralizedSparseEmbedding, generalized_dims, make_generalized_sparse_embedding
 from .shim import install, uninstall
 
 __version__ = "0.1.0"

@@ -9,3 +9,8 @@ SPARSE_DIM_FLOOR = 4
 # leverage.py:100-107 and :87 (JL probe width)
 LEVERAGE_F_C = 40.0
 LEVERAGE_JL_C = 16.0
+
+# generalized sparse embedding dims (sketch.py:69-80, _constants.py:13-19)
+GEN_K_C = 1.0
+GEN_V_C = 1.0
+GEN_Q_C = 1.0

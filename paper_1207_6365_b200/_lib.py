@@ -47,6 +47,10 @@ EXPORTS = (
     "skt_residual_csr",
     "skt_srht_workspace",
     "skt_srht_apply",
+    "skt_gse_buckets",
+    "skt_gse_fold_rows",
+    "skt_gse_apply_dense",
+    "skt_gse_apply_csr",
 )
 
 
@@ -115,7 +119,11 @@ def lib() -> ctypes.CDLL:
         "skt_residual_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, i64, P, P, sz, P], i32),
         "skt_residual_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, i64, P, P, sz, P], i32),
         "skt_srht_workspace": ([i64, i64, ctypes.POINTER(sz)], i32),
-        "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),  # noqa: E501
+        "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),
+        "skt_gse_buckets": ([P, P, i64, i32, u32, u64, P, P], i32),
+        "skt_gse_fold_rows": ([P, i64, i64, P], i32),
+        "skt_gse_apply_dense": ([P, P, u64, P, i32, i64, i64, ctypes.c_double, P, i64, P, P], i32),
+        "skt_gse_apply_csr": ([P, P, u64, P, i32, P, i32, P, i32, i64, ctypes.c_double, P, i64, P], i32),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

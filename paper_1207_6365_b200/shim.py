@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import importlib
 
+from . import generalized as _gen
 from . import sketch as _gpu
 
 _saved: dict = {}
@@ -22,13 +23,18 @@ _saved: dict = {}
 def install() -> None:
     ref = importlib.import_module("sketchnla.sketch")
     low = importlib.import_module("sketchnla.lowrank")
+    lp = importlib.import_module("sketchnla.lp")
     if not _saved:
         _saved["SparseEmbedding"] = ref.SparseEmbedding
         _saved["apply_right"] = ref.apply_right
         _saved["low.apply_right"] = low.apply_right
+        _saved["GeneralizedSparseEmbedding"] = ref.GeneralizedSparseEmbedding
+        _saved["lp.GeneralizedSparseEmbedding"] = lp.GeneralizedSparseEmbedding
     ref.SparseEmbedding = _gpu.SparseEmbedding
     ref.apply_right = _gpu.apply_right
     low.apply_right = _gpu.apply_right
+    ref.GeneralizedSparseEmbedding = _gen.GeneralizedSparseEmbedding
+    lp.GeneralizedSparseEmbedding = _gen.GeneralizedSparseEmbedding
 
 
 def uninstall() -> None:
@@ -36,7 +42,10 @@ def uninstall() -> None:
         return
     ref = importlib.import_module("sketchnla.sketch")
     low = importlib.import_module("sketchnla.lowrank")
+    lp = importlib.import_module("sketchnla.lp")
     ref.SparseEmbedding = _saved["SparseEmbedding"]
     ref.apply_right = _saved["apply_right"]
     low.apply_right = _saved["low.apply_right"]
+    ref.GeneralizedSparseEmbedding = _saved["GeneralizedSparseEmbedding"]
+    lp.GeneralizedSparseEmbedding = _saved["lp.GeneralizedSparseEmbedding"]
     _saved.clear()

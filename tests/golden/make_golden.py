@@ -215,6 +215,31 @@ def srht_cases():
     np.savez_compressed(os.path.join(HERE, "srht_cases.npz"), **out)
 
 
+def gse_cases():
+    """GeneralizedSparseEmbedding (sketch.py:176-238): its hashes and S.A on
+    dense (fp64, fp32, 1-D) and CSR (canonical and with duplicate columns)."""
+    g = np.random.default_rng(4242)
+    out, meta = {}, []
+    for k, (n, r, eps, delta, seed) in enumerate([(3000, 4, 0.5, 0.1, 7), (5000, 3, 0.4, 0.2, 11), (17, 2, 0.5, 0.5, 1)]):
+        op = RS.GeneralizedSparseEmbedding(n, r, eps, delta, seed)
+        out[f"outer{k}"] = op.outer_bucket.astype(np.uint32)
+        out[f"inner{k}"] = op.inner_bucket.astype(np.uint32)
+        out[f"sign{k}"] = op.inner_sign.astype(np.int8)
+        a64 = g.standard_normal((n, 5))
+        a32 = g.standard_normal((n, 7)).astype(np.float32)
+        a1 = g.standard_normal(n)
+        ac = sp.csr_array(sp.random_array((n, 40), density=0.1, rng=g, format="csr"))
+        dup = sp.csr_array((np.array([1.5, -2.0, 0.25, 3.0]), np.array([3, 3, 0, 3]), np.array([0, 2, 4] + [4] * (n - 2))),
+                           shape=(n, 5))
+        out[f"a64_{k}"], out[f"a32_{k}"], out[f"a1_{k}"] = a64, a32, a1
+        out[f"ac_indptr{k}"], out[f"ac_indices{k}"], out[f"ac_data{k}"] = ac.indptr, ac.indices, ac.data
+        out[f"sa64_{k}"], out[f"sa32_{k}"], out[f"sa1_{k}"] = op.apply(a64), op.apply(a32), op.apply(a1)
+        out[f"sac_{k}"], out[f"sadup_{k}"] = op.apply(ac), op.apply(dup)
+        meta.append([n, r, eps, delta, seed, op.q, op.k_blocks, op.v, op.output_dim])
+    out["meta"] = np.asarray(meta, dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "gse_cases.npz"), **out)
+
+
 def seeds():
     rows = []
     for seed, key in [(0, ()), (1, (0, 0)), (1, (0, 1)), (5, (3,)), (2**40 + 17, (0, 0)),
@@ -232,6 +257,7 @@ if __name__ == "__main__":
     assert "reference" in os.path.dirname(sketchnla.__file__), sketchnla.__file__
     seeds()
     srht_cases()
+    gse_cases()
     hash_cases()
     apply_cases()
     configs()

@@ -68,6 +68,9 @@ def test_shim_rebinds_reference_module_globals():
     try:
         assert ref.SparseEmbedding is skb.SparseEmbedding
         assert ref.apply_right is skb.apply_right and low.apply_right is skb.apply_right
+        lp = importlib.import_module("sketchnla.lp")
+        assert ref.GeneralizedSparseEmbedding is skb.GeneralizedSparseEmbedding
+        assert lp.GeneralizedSparseEmbedding is skb.GeneralizedSparseEmbedding
         # the reference factories resolve the class at call time (sketch.py:400,426,465)
         if not torch.cuda.is_available():
             with pytest.raises(Exception):
