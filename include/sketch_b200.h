@@ -210,6 +210,29 @@ skt_status skt_gse_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64
                              const void *a_vals, skt_dtype val_dtype, int64_t d, double weight, double *sa,
                              int64_t ldsa, void *stream);
 
+/* ---- Matrix Market ingest ------------------------------------------------- */
+/* Replaces load_matrix_market (io.py:37-104).  skt_mm_probe reads the header
+ * and size line; skt_mm_read_coo parses the coordinate entries on n_threads
+ * host threads (0 = all cores) into caller host arrays (0-based, capacity >=
+ * n_entries, x2 for symmetric storage, which is expanded as the reference
+ * does), with the reference's "path:line: reason" errors (SKT_EINVAL).
+ * skt_coo_to_csr canonicalises on the device (io.py:101-102 -> as_csr,
+ * _validation.py:30-41): (row, col)-sorted, duplicates summed in file order,
+ * zero sums dropped; indptr (n_rows + 1, int64), indices (int32), values
+ * (fp64, capacity count), *nnz (device int64). */
+typedef struct skt_mm_info {
+  int64_t n_rows, n_cols, n_entries;
+  int32_t field;     /* 0 real, 1 integer, 2 pattern */
+  int32_t symmetric; /* 0 general, 1 symmetric */
+} skt_mm_info;
+skt_status skt_mm_probe(const char *path, skt_mm_info *info);
+skt_status skt_mm_read_coo(const char *path, int64_t capacity, int64_t *rows, int64_t *cols, double *vals,
+                           int64_t *count, int32_t n_threads);
+skt_status skt_coo_to_csr_workspace(int64_t count, int64_t n_rows, int64_t n_cols, size_t *bytes);
+skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, const double *vals, int64_t count,
+                          int64_t n_rows, int64_t n_cols, int64_t *indptr, int32_t *indices, double *out_vals,
+                          int64_t *nnz, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,7 +51,21 @@ EXPORTS = (
     "skt_gse_fold_rows",
     "skt_gse_apply_dense",
     "skt_gse_apply_csr",
+    "skt_mm_probe",
+    "skt_mm_read_coo",
+    "skt_coo_to_csr_workspace",
+    "skt_coo_to_csr",
 )
+
+
+class SktMmInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_rows", ctypes.c_int64),
+        ("n_cols", ctypes.c_int64),
+        ("n_entries", ctypes.c_int64),
+        ("field", ctypes.c_int32),
+        ("symmetric", ctypes.c_int32),
+    ]
 
 
 class SktPcg64(ctypes.Structure):
@@ -124,6 +138,10 @@ def lib() -> ctypes.CDLL:
         "skt_gse_fold_rows": ([P, i64, i64, P], i32),
         "skt_gse_apply_dense": ([P, P, u64, P, i32, i64, i64, ctypes.c_double, P, i64, P, P], i32),
         "skt_gse_apply_csr": ([P, P, u64, P, i32, P, i32, P, i32, i64, ctypes.c_double, P, i64, P], i32),
+        "skt_mm_probe": ([ctypes.c_char_p, ctypes.POINTER(SktMmInfo)], i32),
+        "skt_mm_read_coo": ([ctypes.c_char_p, i64, P, P, P, ctypes.POINTER(i64), i32], i32),
+        "skt_coo_to_csr_workspace": ([i64, i64, i64, ctypes.POINTER(sz)], i32),
+        "skt_coo_to_csr": ([P, P, P, i64, i64, i64, P, P, P, P, P, sz, P], i32),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

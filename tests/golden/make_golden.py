@@ -240,6 +240,38 @@ def gse_cases():
     np.savez_compressed(os.path.join(HERE, "gse_cases.npz"), **out)
 
 
+def mm_cases():
+    """load_matrix_market (io.py:37-104) on the texts of tests/golden/mm_cases.py:
+    canonical CSR arrays, and the error message for each malformed file."""
+    import tempfile
+
+    from sketchnla.io import load_matrix_market
+
+    from tests.golden.mm_cases import BAD, GOOD
+
+    out, errors = {}, {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, text in GOOD.items():
+            p = os.path.join(tmp, f"{name}.mtx")
+            with open(p, "w") as f:
+                f.write(text)
+            m = load_matrix_market(p)
+            out[f"{name}_indptr"], out[f"{name}_indices"], out[f"{name}_data"] = m.indptr, m.indices, m.data
+            out[f"{name}_shape"] = np.asarray(m.shape)
+        for name, text in BAD.items():
+            p = os.path.join(tmp, f"{name}.mtx")
+            with open(p, "w") as f:
+                f.write(text)
+            try:
+                load_matrix_market(p)
+                errors[name] = None
+            except ValueError as e:
+                errors[name] = str(e).replace(p, "{path}")
+    np.savez_compressed(os.path.join(HERE, "mm_cases.npz"), **out)
+    with open(os.path.join(HERE, "mm_errors.json"), "w") as f:
+        json.dump(errors, f, indent=1)
+
+
 def seeds():
     rows = []
     for seed, key in [(0, ()), (1, (0, 0)), (1, (0, 1)), (5, (3,)), (2**40 + 17, (0, 0)),
@@ -258,6 +290,7 @@ if __name__ == "__main__":
     seeds()
     srht_cases()
     gse_cases()
+    mm_cases()
     hash_cases()
     apply_cases()
     configs()
