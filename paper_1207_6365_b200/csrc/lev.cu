@@ -161,7 +161,7 @@ skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, co
     const int dk8 = (int)((d + 7) & ~7LL);  // K of the MMA chain
     const size_t smem = lev_tc_smem(dk8, (int)k);
     if (smem <= 200 * 1024) {
-      auto kern = lev_tc_kernel<IP, IX, TS>;
+      auto kern = tc_merged((int)k) ? lev_tc_kernel<IP, IX, TS, true> : lev_tc_kernel<IP, IX, TS, false>;
       SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
       const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
       // resident CTAs per SM: bounded by shared memory and by the 512 TMEM

@@ -65,10 +65,38 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
-// TMEM columns a CTA allocates for a k-wide accumulator
-__host__ __device__ inline uint32_t lev_tc_cols(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : k <= 128 ? 128 : 256; }
+// A tile offsets / descriptors (K-major, no swizzle).  The 128-byte-swizzled
+// layout was measured: faster MMAs in isolation (tools/lev_prof.cu), but 4%
+// slower in this kernel (the scatter's extra address math), so not used.
+__device__ __forceinline__ uint32_t tc_a_off(int r, int c) { return tc_off(r, c, kTcRows); }
+__device__ __forceinline__ uint64_t tc_a_desc(uint32_t base, int ks) {  // K step ks (8 elements)
+  return tc_desc(base + (uint32_t)ks * 2 * (kTcRows * 16), kTcRows * 16, 128);
+}
+// Merged probe operand (k % 32 == 0, 2k <= 256): P staged as one 2k-row
+// operand [P_hi; P_lo], A_hi.[P_hi | P_lo] is one N = 2k MMA and A_lo.P_hi
+// accumulates into columns 0..k-1 -- 16 instead of 24 MMAs per 128 x 64 tile
+// (-6% on config 4); the epilogue adds columns c and k + c.
+__host__ __device__ inline bool tc_merged(int k) { return k % 32 == 0 && 2 * k <= 256; }
 
-template <typename IP, typename IX, typename TS>
+// 32 TMEM columns of this warp's 32 lanes
+#define TC_TMEM_LD32(taddr, v)                                                                            \
+  asm volatile(                                                                                           \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"   \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                         \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),  \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),         \
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),       \
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),       \
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                            \
+      : "r"(taddr))
+
+// TMEM columns a CTA allocates for a k-wide accumulator
+__host__ __device__ inline uint32_t lev_tc_cols(int k) {
+  const int c = tc_merged(k) ? 2 * k : k;
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : 256;
+}
+
+template <typename IP, typename IX, typename TS, bool kMerged>
 __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, int dk,
                                                             const IP *__restrict__ aip,
                                                             const IX *__restrict__ aix,
@@ -86,6 +114,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
   float *a_lo = (float *)(smem + a_bytes);
   float *p_hi = (float *)(smem + 2 * a_bytes);
   float *p_lo = (float *)(smem + 2 * a_bytes + p_bytes);
+  constexpr bool merged = kMerged;  // host selects tc_merged(k)
 
   // ---- one-time setup: zero A tiles, stage P^T (K-major: row = probe column)
   for (uint32_t i = tid; i < 2 * a_bytes / 16; i += kTcThreads) ((uint4 *)smem)[i] = make_uint4(0, 0, 0, 0);
@@ -94,9 +123,14 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
     const double p = kk < d ? probe[(int64_t)kk * k + col] : 0.0;
     const float hi = tf32_hi((float)p);
     const float lo = tf32_hi((float)(p - (double)hi));
-    const uint32_t off = tc_off(col, kk, k);
-    *(float *)((unsigned char *)p_hi + off) = hi;
-    *(float *)((unsigned char *)p_lo + off) = lo;
+    if (merged) {  // one 2k-row operand at p_hi
+      *(float *)((unsigned char *)p_hi + tc_off(col, kk, 2 * k)) = hi;
+      *(float *)((unsigned char *)p_hi + tc_off(k + col, kk, 2 * k)) = lo;
+    } else {
+      const uint32_t off = tc_off(col, kk, k);
+      *(float *)((unsigned char *)p_hi + off) = hi;
+      *(float *)((unsigned char *)p_lo + off) = lo;
+    }
   }
   if (warp == 0) {
     const uint32_t ncols = lev_tc_cols(k);
@@ -175,7 +209,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
   auto put = [&](int trow, int c, float v) {
     const float hi = tf32_hi(v);
     const float lo = tf32_hi(v - hi);
-    const uint32_t off = tc_off(trow, c, kTcRows);
+    const uint32_t off = tc_a_off(trow, c);
     *(float *)((unsigned char *)a_hi + off) = hi;
     *(float *)((unsigned char *)a_lo + off) = lo;
   };
@@ -232,7 +266,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
       if (r < n) {
         const int64_t rb = (int64_t)aip[r], re = (int64_t)aip[r + 1];
         for (int64_t q = rb; q < re; ++q) {
-          const uint32_t off = tc_off(tid, (int)aix[q], kTcRows);
+          const uint32_t off = tc_a_off(tid, (int)aix[q]);
           float *h = (float *)((unsigned char *)a_hi + off);
           float *l = (float *)((unsigned char *)a_lo + off);
           const float v = av[q] + (*h + *l);
@@ -254,9 +288,16 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
       const uint32_t ph = tc_smem_u32(p_hi), pl = tc_smem_u32(p_lo);
       for (int ks = 0; ks < dk / 8; ++ks) {
         const uint32_t oa = (uint32_t)ks * 2 * lbo_a, op = (uint32_t)ks * 2 * lbo_p;
-        tc_mma(tmem, tc_desc(ah + oa, lbo_a, 128), tc_desc(ph + op, lbo_p, 128), idesc, ks > 0);
-        tc_mma(tmem, tc_desc(ah + oa, lbo_a, 128), tc_desc(pl + op, lbo_p, 128), idesc, 1);
-        tc_mma(tmem, tc_desc(al + oa, lbo_a, 128), tc_desc(ph + op, lbo_p, 128), idesc, 1);
+        if (merged) {
+          const uint32_t lbo_p2 = 2 * lbo_p, op2 = (uint32_t)ks * 2 * lbo_p2;
+          tc_mma(tmem, tc_a_desc(ah, ks), tc_desc(ph + op2, lbo_p2, 128), tc_idesc(2 * k), ks > 0);
+          tc_mma(tmem, tc_a_desc(al, ks), tc_desc(ph + op2, lbo_p2, 128), idesc, 1);
+        } else {
+          tc_mma(tmem, tc_a_desc(ah, ks), tc_desc(ph + op, lbo_p, 128), idesc, ks > 0);
+          tc_mma(tmem, tc_a_desc(ah, ks), tc_desc(pl + op, lbo_p, 128), idesc, 1);
+          tc_mma(tmem, tc_a_desc(al, ks), tc_desc(ph + op, lbo_p, 128), idesc, 1);
+        }
+        (void)oa;
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        tc_smem_u32(&mbar))
@@ -285,21 +326,19 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
     for (int c0 = 0; c0 < k; c0 += 32) {
       uint32_t v[32];
       const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
-            "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
-            "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
+      uint32_t w2[kMerged ? 32 : 1];
+      TC_TMEM_LD32(taddr, v);
+      if constexpr (kMerged) TC_TMEM_LD32(taddr + (uint32_t)k, w2);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       const int cn = k - c0 < 32 ? k - c0 : 32;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (j < cn) {
-          const double x = (double)__uint_as_float(v[j]);
+          double x;
+          if constexpr (kMerged)
+            x = (double)(__uint_as_float(v[j]) + __uint_as_float(w2[j]));
+          else
+            x = (double)__uint_as_float(v[j]);
           sc = fma(x, x, sc);
         }
       }
@@ -310,7 +349,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       if (cur_c[i] >= 0) {
-        const uint32_t off = tc_off(warp * 32 + (i / 2) * S + g, cur_c[i], kTcRows);
+        const uint32_t off = tc_a_off(warp * 32 + (i / 2) * S + g, cur_c[i]);
         *(float *)((unsigned char *)a_hi + off) = 0.f;
         *(float *)((unsigned char *)a_lo + off) = 0.f;
       }
@@ -320,7 +359,7 @@ __global__ void __launch_bounds__(kTcThreads) lev_tc_kernel(int64_t n, int d, in
     for (uint32_t m = longz; m; m &= m - 1) {
       const int r = __ffs(m) - 1;
       for (int c = lane; c < dk; c += 32) {
-        const uint32_t off = tc_off(warp * 32 + r, c, kTcRows);
+        const uint32_t off = tc_a_off(warp * 32 + r, c);
         *(float *)((unsigned char *)a_hi + off) = 0.f;
         *(float *)((unsigned char *)a_lo + off) = 0.f;
       }

@@ -149,7 +149,7 @@ int main(int argc, char **argv) {
   float ms;
   // v1
   const size_t s1 = lev_tc_smem(dk, k);
-  auto k1 = lev_tc_kernel<int, int, double>;
+  auto k1 = lev_tc_kernel<int, int, double, true>;  // k = 32: merged probe operand
   CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
   const int64_t b1 = std::min<int64_t>(ntiles, 148 * 2);
   for (int i = 0; i < 3; ++i) k1<<<b1, kTcThreads, s1>>>(n, d, dk, dip, dix, dv, dp, k, ds1);
