@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "lev_tc.cuh"
 #include "lev_tc2.cuh"
+#include "lev_tc3.cuh"
 
 namespace skt {
 namespace {
@@ -23,6 +24,14 @@ namespace {
 inline bool lev_tc_enabled() {
   static const bool on = [] {
     const char *e = getenv("SKT_LEV_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// SKT_LEV_TC3=0 keeps k % 32 == 0 shapes on the 3xTF32 kernel (lev_tc.cuh).
+inline bool lev_tc3_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_LEV_TC3");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -159,6 +168,18 @@ skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, co
       return check_launch(fn);
     }
     const int dk8 = (int)((d + 7) & ~7LL);  // K of the MMA chain
+    const size_t smem3 = lev_tc3_smem(dk8, (int)k);
+    if (lev_tc3_enabled() && tc3_ok((int)k) && smem3 <= 200 * 1024) {  // scaled 2xFP16 (lev_tc3.cuh)
+      auto kern = lev_tc3_kernel<IP, IX, TS>;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3), fn);
+      const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
+      const size_t by_tmem = 512 / tc3_cols((int)k);
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>(4, by_tmem), (220 * 1024) / smem3));
+      const int64_t blocks = std::min<int64_t>(ntiles, (int64_t)kNumSMs * per_sm);
+      SKT_LAUNCH(kern, (unsigned)blocks, kTcThreads, smem3, st, n, (int)d, dk8, (const IP *)aip,
+                 (const IX *)aix, (const float *)av, p, (int)k, (TS *)scores);
+      return check_launch(fn);
+    }
     const size_t smem = lev_tc_smem(dk8, (int)k);
     if (smem <= 200 * 1024) {
       auto kern = tc_merged((int)k) ? lev_tc_kernel<IP, IX, TS, true> : lev_tc_kernel<IP, IX, TS, false>;

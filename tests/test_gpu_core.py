@@ -386,13 +386,36 @@ def test_lev_tensor_core_3xtf32(n, d, k, density, rng):
     assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-5
 
 
-@pytest.mark.parametrize("d", [64, 128])  # 64: staged v2 kernel, 128: register-staged v1
-def test_lev_tensor_core_noncanonical_rows(d, rng):
+@pytest.mark.parametrize("k", [32, 64, 128])
+def test_lev_tensor_core_row_scaling_extremes(k, rng):
+    """The scaled 2xFP16 kernel (lev_tc3.cuh, k % 32 == 0): rows spanning 1e-30 ..
+    1e30, entries inside a row spanning 1e-6, empty rows, a 300-entry row, a
+    partial last tile -- 1e-5 relative to the fp64 oracle."""
+    from paper_1207_6365_b200.solvers import lev_rownorms
+
+    n, d = 9_001, 300
+    a = sp.random_array((n, d), density=0.05, rng=rng, format="csr").tolil()
+    a[7, :] = rng.standard_normal(d)  # one full row (long-row path, > 80 entries)
+    a[11, :] = 0  # empty row
+    a = sp.csr_array(a)
+    row_scale = 10.0 ** rng.uniform(-30, 30, n)
+    a = sp.csr_array(sp.diags_array(row_scale) @ a, dtype=np.float32)
+    a.data *= np.where(rng.random(a.nnz) < 0.1, 1e-6, 1.0).astype(np.float32)
+    probe = rng.standard_normal((d, k)) * 1e3
+    ref = O.lev_rownorms_csr(a, probe)
+    got = lev_rownorms(a, probe)
+    nz = ref > 0
+    assert np.all(got[~nz] == 0)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-5
+
+
+@pytest.mark.parametrize("d,k", [(64, 32), (128, 32), (64, 40)])  # k=32: lev_tc3.cuh, k=40: lev_tc.cuh
+def test_lev_tensor_core_noncanonical_rows(d, k, rng):
     """Duplicate and unsorted column indices are summed like scipy's a @ probe
     (the dirty-tile rebuild), on both tensor-core kernels."""
     from paper_1207_6365_b200.solvers import lev_rownorms
 
-    n, k = 3_000, 32
+    n = 3_000
     counts = rng.integers(0, 40, size=n)
     indptr = np.concatenate([[0], np.cumsum(counts)])
     indices = np.concatenate([np.sort(rng.choice(d, size=c, replace=False)) for c in np.minimum(counts, d)])
