@@ -95,7 +95,15 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
   uint32_t phase = 0;
 
   const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
-  constexpr int G = 8, S = 32 / G, E = 16;  // 8 lanes per row, <= 16 staged nonzeros per lane
+#ifndef SKT_TC3_G
+#define SKT_TC3_G 8
+#endif
+  // G lanes per row, S = 32/G rows per warp instruction, NI = G row iterations
+  // per warp, JP = 16/G staged nonzeros per lane and row: the first NR = 16
+  // nonzeros of every row are staged (E = 16 registers per lane).  G = 4 (8
+  // rows of distinct row mod 8 per store: no bank conflicts) measured 5%
+  // slower than G = 8 on config 4 (less coalesced loads, more shuffles).
+  constexpr int G = SKT_TC3_G, S = 32 / G, NI = G, JP = 16 / G, E = 16, NR = 16;
   const int g = lane / G, gl = lane % G;
   auto load_desc = [&](int64_t tile, int64_t &rs, int &len) {
     const int64_t row = tile * kTcRows + warp * 32 + lane;
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
   float lv[2];
   auto load_data = [&](int64_t rs, int len) {
     {
-      const uint32_t lm = __ballot_sync(0xffffffffu, len > 2 * G);
+      const uint32_t lm = __ballot_sync(0xffffffffu, len > NR);
       lr = lm ? __ffs(lm) - 1 : -1;
       lc[0] = lc[1] = -1;
       if (lm) {
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
         const int len_r = __shfl_sync(0xffffffffu, len, lr);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int q = 2 * G + lane + 32 * j;
+          const int q = NR + lane + 32 * j;
           if (q < len_r) {
             lc[j] = (int)__ldg(aix + rs_r + q);
             lv[j] = __ldg(av + rs_r + q);
@@ -132,17 +140,17 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
       }
     }
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
+    for (int i = 0; i < NI; ++i) {
       const int r = i * S + g;
       const int64_t rs_r = __shfl_sync(0xffffffffu, rs, r);
       const int len_r = __shfl_sync(0xffffffffu, len, r);
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < JP; ++j) {
         const int q = gl + G * j;
-        pc[2 * i + j] = -1;
+        pc[i * JP + j] = -1;
         if (q < len_r) {
-          pc[2 * i + j] = (int)__ldg(aix + rs_r + q);
-          pv[2 * i + j] = __ldg(av + rs_r + q);
+          pc[i * JP + j] = (int)__ldg(aix + rs_r + q);
+          pv[i * JP + j] = __ldg(av + rs_r + q);
         }
       }
     }
@@ -156,14 +164,15 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
   load_desc(tile + gridDim.x, rs_n, len_n);
   for (; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * kTcRows;
-    const uint32_t longm = __ballot_sync(0xffffffffu, len_c > 2 * G);
+    const uint32_t longm = __ballot_sync(0xffffffffu, len_c > NR);
     // ---- per-row max |a| (registers, then the long rows' tails) -> scale
-    float m[E / 2];
+    float m[NI];
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
+    for (int i = 0; i < NI; ++i) {
       m[i] = 0.f;
-      if (pc[2 * i] >= 0) m[i] = fabsf(pv[2 * i]);
-      if (pc[2 * i + 1] >= 0) m[i] = fmaxf(m[i], fabsf(pv[2 * i + 1]));
+#pragma unroll
+      for (int j = 0; j < JP; ++j)
+        if (pc[i * JP + j] >= 0) m[i] = fmaxf(m[i], fabsf(pv[i * JP + j]));
     }
     if (longm) {
       for (uint32_t mm = longm; mm; mm &= mm - 1) {  // max over each long row's tail (whole warp)
@@ -176,17 +185,17 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
           for (int j = 0; j < 2; ++j)
             if (lc[j] >= 0) t = fmaxf(t, fabsf(lv[j]));
         }
-        for (int q = (r == lr ? 2 * G + 64 : 2 * G) + lane; q < len_r; q += 32) t = fmaxf(t, fabsf(__ldg(av + rs_r + q)));
+        for (int q = (r == lr ? NR + 64 : NR) + lane; q < len_r; q += 32) t = fmaxf(t, fabsf(__ldg(av + rs_r + q)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, o));
         // fold into the row's group: row r = 4i + g
 #pragma unroll
-        for (int i = 0; i < E / 2; ++i)
+        for (int i = 0; i < NI; ++i)
           if (i * S + g == r) m[i] = fmaxf(m[i], t);
       }
     }
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
+    for (int i = 0; i < NI; ++i) {
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) m[i] = fmaxf(m[i], __shfl_xor_sync(0xffffffffu, m[i], o, G));
       if (gl == 0) rexp[warp * 32 + i * S + g] = t2_exp(m[i]);
@@ -195,21 +204,23 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
     // ---- column order check (duplicates / unsorted rows -> rebuild below)
     bool dirty = false;
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
-      const int p0 = __shfl_up_sync(0xffffffffu, pc[2 * i], 1, G);
-      const int p7 = __shfl_sync(0xffffffffu, pc[2 * i], G - 1, G);
-      const int p1 = __shfl_up_sync(0xffffffffu, pc[2 * i + 1], 1, G);
-      if (gl > 0 && pc[2 * i] >= 0) dirty |= pc[2 * i] <= p0;
-      if (pc[2 * i + 1] >= 0) dirty |= pc[2 * i + 1] <= (gl > 0 ? p1 : p7);
+    for (int i = 0; i < NI; ++i) {
+#pragma unroll
+      for (int j = 0; j < JP; ++j) {  // predecessor of entry gl + G j: lane gl - 1 (same j) or lane G - 1 (j - 1)
+        const int c = pc[i * JP + j];
+        const int ps = __shfl_up_sync(0xffffffffu, c, 1, G);
+        const int pw = j > 0 ? __shfl_sync(0xffffffffu, pc[i * JP + j - 1], G - 1, G) : -1;
+        if (c >= 0 && (gl > 0 || j > 0)) dirty |= c <= (gl > 0 ? ps : pw);
+      }
     }
     // ---- densify: one packed (hi, lo) word per nonzero
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
+    for (int i = 0; i < NI; ++i) {
       const int r = warp * 32 + i * S + g;
       const float sc = __int_as_float((127 - rexp[r]) << 23);
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
-        if (pc[2 * i + j] >= 0) aw[tc_off(r, pc[2 * i + j], kTcRows) >> 2] = t2_pack(pv[2 * i + j] * sc);
+      for (int j = 0; j < JP; ++j)
+        if (pc[i * JP + j] >= 0) aw[tc_off(r, pc[i * JP + j], kTcRows) >> 2] = t2_pack(pv[i * JP + j] * sc);
     }
     if (lr >= 0) {
       const int64_t rs_r = __shfl_sync(0xffffffffu, rs_c, lr);
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         if (lc[j] >= 0) {
-          dirty |= lc[j] <= (int)__ldg(aix + rs_r + 2 * G + lane + 32 * j - 1);
+          dirty |= lc[j] <= (int)__ldg(aix + rs_r + NR + lane + 32 * j - 1);
           aw[tc_off(warp * 32 + lr, lc[j], kTcRows) >> 2] = t2_pack(lv[j] * sc);
         }
     }
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
       const int64_t rs_r = __shfl_sync(0xffffffffu, rs_c, r);
       const int len_r = __shfl_sync(0xffffffffu, len_c, r);
       const float sc = __int_as_float((127 - rexp[warp * 32 + r]) << 23);
-      for (int q = (r == lr ? 2 * G + 64 : 2 * G) + lane; q < len_r; q += 32) {
+      for (int q = (r == lr ? NR + 64 : NR) + lane; q < len_r; q += 32) {
         const int c = (int)__ldg(aix + rs_r + q);
         dirty |= c <= (int)__ldg(aix + rs_r + q - 1);
         aw[tc_off(warp * 32 + r, c, kTcRows) >> 2] = t2_pack(__ldg(av + rs_r + q) * sc);
@@ -307,7 +318,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
     // ---- re-zero what this tile wrote
 #pragma unroll
     for (int i = 0; i < E; ++i)
-      if (cur_c[i] >= 0) aw[tc_off(warp * 32 + (i / 2) * S + g, cur_c[i], kTcRows) >> 2] = 0u;
+      if (cur_c[i] >= 0) aw[tc_off(warp * 32 + (i / JP) * S + g, cur_c[i], kTcRows) >> 2] = 0u;
     for (uint32_t mm = longz; mm; mm &= mm - 1) {
       const int r = __ffs(mm) - 1;
       for (int c = lane; c < dk; c += 32) aw[tc_off(warp * 32 + r, c, kTcRows) >> 2] = 0u;
