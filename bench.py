@@ -356,6 +356,8 @@ def our_arm(args, cfg):
     r0, r1 = (0, n) if bucket_mode else (rank * n // world, (rank + 1) * n // world)
     b0, b1 = (rank * m // world, (rank + 1) * m // world) if bucket_mode else (0, m)
     sa_dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
+    if args.exact and cfg.get("fast"):
+        sa_dt = torch.float64  # the deterministic wide-d kernel accumulates in the fp64 output row
 
     # ---- inputs resident in HBM
     if cfg["kind"] == "dense":
@@ -410,7 +412,7 @@ def our_arm(args, cfg):
             op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
         else:
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
-                                 deterministic=not cfg.get("fast", False),
+                                 deterministic=args.exact or not cfg.get("fast", False),
                                  buckets=(b0, b1) if bucket_mode else None)
 
     # N > 1, dense: pipelined exchange -- SA is computed in contiguous bucket
@@ -581,6 +583,8 @@ def main():
     ap.add_argument("--kernel", default="sa", choices=["sa", "lev", "lowrank"],
                     help="sa: the S.A hot path (headline); lev: K5 leverage contraction (config c4); "
                          "lowrank: config 5 low-rank error ratio")
+    ap.add_argument("--exact", action="store_true",
+                    help="bit-exact deterministic kernels also for configs that default to fast mode (c5)")
     ap.add_argument("--chunks", type=int, default=4,
                     help="N > 1: bucket ranges whose all-reduce overlaps the next range's compute")
     ap.add_argument("--e2e-steps", type=int, default=3)
