@@ -7,6 +7,8 @@ python bench.py > gpurun_out/final/bench_c3.json 2> gpurun_out/final/bench_c3.er
 python bench.py --impl reference > gpurun_out/final/ref_c3.json 2> gpurun_out/final/ref_c3.err; echo rc_ref=$?
 for c in c1 c2 c4 c5; do python bench.py --config $c --no-e2e --no-cpu-baseline > gpurun_out/final/bench_$c.json 2> gpurun_out/final/bench_$c.err; echo rc_$c=$?; done
 python bench.py --config c4 --kernel lev --no-e2e --no-cpu-baseline > gpurun_out/final/bench_c4_lev.json 2> gpurun_out/final/bench_c4_lev.err; echo rc_lev=$?
+python bench.py --config c5 --exact --no-e2e --no-cpu-baseline > gpurun_out/final/bench_c5_exact.json 2> gpurun_out/final/bench_c5_exact.err; echo rc_c5x=$?
+timeout 300 python tools/srht_time.py > gpurun_out/final/srht_time.txt 2>&1; echo rc_srht=$?
 timeout 300 tools/gather_bench > gpurun_out/final/gather_bench.txt 2>&1; echo rc_gather=$?
 nproc > gpurun_out/final/nproc.txt; nvidia-smi -q | head -40 > gpurun_out/final/nvsmi.txt
 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/plain.log 2>&1 && \
@@ -15,4 +17,4 @@ ncu --set full --clock-control none --import-source on -k regex:apply_dense -s 3
 python bench.py --config c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/plain_c4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:csr_ -s 3 -c 1 -o gpurun_out/final/prof_c4 python bench.py --config c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_c4.log 2>&1; echo rc_ncu3=$?
 python bench.py --config c4 --kernel lev --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/plain_lev.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:lev_tc -s 3 -c 1 -o gpurun_out/final/prof_lev python bench.py --config c4 --kernel lev --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_lev.log 2>&1; echo rc_ncu4=$?
+ncu --set full --clock-control none --import-source on -k regex:lev_tc3 -s 3 -c 1 -o gpurun_out/final/prof_lev python bench.py --config c4 --kernel lev --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/final/ncu_lev.log 2>&1; echo rc_ncu4=$?
