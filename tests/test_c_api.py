@@ -42,3 +42,27 @@ def test_c_demo_matches_oracle(tmp_path):
     sa = O.apply_dense(h, s, t, a)
     assert [int(x) for x in lines["bucket[0..3]"].split()] == h[:4].tolist()
     assert [float(x) for x in lines["SA[0][0..3] "].split()] == sa[0].tolist()
+
+
+def test_c_mm_ingest_demo(tmp_path):
+    """Matrix Market ingest from plain C (host only: runs without a GPU)."""
+    if not os.path.exists("/usr/local/cuda/include/cuda_runtime.h"):
+        pytest.skip("CUDA headers not installed")
+    exe = str(tmp_path / "mm_demo")
+    lib_dir = os.path.join(ROOT, "paper_1207_6365_b200")
+    cmd = ["gcc", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "examples", "mm_ingest_demo.c"),
+           "-o", exe, "-L", lib_dir, "-lsketch_b200", f"-Wl,-rpath,{lib_dir}"]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    good = tmp_path / "s.mtx"
+    good.write_text("%%MatrixMarket matrix coordinate real symmetric\n% c\n3 3 3\n1 1 2.5\n3 1 -1e-3\n2 2 4\n")
+    out = subprocess.run([exe, str(good), "2"], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    lines = dict(line.split(" = ") for line in out.stdout.splitlines())
+    assert lines["shape"] == "3 3" and lines["declared"] == "3" and lines["count"] == "4"
+    assert lines["field symmetric"] == "0 1"
+    assert lines["entry1"] == "2 0 -0.001"
+    bad = tmp_path / "b.mtx"
+    bad.write_text("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 9 1.0\n")
+    out = subprocess.run([exe, str(bad)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 1 and out.stdout.strip() == f"error = {bad}:3: index out of range"
