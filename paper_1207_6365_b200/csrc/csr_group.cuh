@@ -83,7 +83,11 @@ __global__ void __launch_bounds__(kGroupWarps * 32) csr_group_kernel(
     const int64_t k2 = k0 + 64;
     const uint32_t wn2 = k2 + lane < end ? __ldg(grow + k2 + lane) : 0u;
     const uint32_t bn2 = k2 + lane < end ? (uint32_t)(gblo ? __ldg(gblo + k2 + lane) : 0) : 0u;
-    // ---- accumulate in row order
+    // ---- accumulate in row order.  Rows of a step (lanes i*S .. i*S+S-1 of
+    // the chunk) that share a bucket serialise that step in row order: one
+    // match over (bucket, step) flags every clashing step of the chunk at once.
+    const uint32_t ckey = lane < nrows ? ((bc & 0xffu) | ((uint32_t)(lane / S) << 8)) : (0x10000u | (uint32_t)lane);
+    const uint32_t clash_lanes = __ballot_sync(0xffffffffu, __popc(__match_any_sync(0xffffffffu, ckey)) > 1);
 #pragma unroll
     for (int i = 0; i < kSteps; ++i) {
       if (i * S < nrows) {  // warp-uniform
@@ -91,18 +95,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) csr_group_kernel(
         const uint32_t pk_r = __shfl_sync(0xffffffffu, pk_c, r);
         const int bl_r = (int)(pk_r & 0xffu);
         const bool neg_r = (pk_r >> 8) != 0;
-        // rows of the step sharing a bucket (or a long row) -> serialise the
-        // step in row order; otherwise all S rows add in one warp step.
-        bool clash = false;
-#pragma unroll
-        for (int j = 1; j < S; ++j) {
-          const uint32_t bj = __shfl_sync(0xffffffffu, pk_c, i * S + j) & 0xffu;
-#pragma unroll
-          for (int q = 0; q < j; ++q) {
-            const uint32_t bq = __shfl_sync(0xffffffffu, pk_c, i * S + q) & 0xffu;
-            clash |= (i * S + j < nrows) && bq == bj;
-          }
-        }
+        const bool clash = ((clash_lanes >> (i * S)) & ((1u << S) - 1u)) != 0;
         const uint32_t steplong = (longm >> (i * S)) & ((1u << S) - 1u);
         const bool serial = clash || steplong != 0;
         const int rank = serial ? g : 0;
