@@ -85,8 +85,15 @@ __device__ __forceinline__ void unscatter_rows(TV *tile, int dp, int lane, const
 
 __device__ __forceinline__ int tile_g(int lmax) { return lmax <= 4 ? 4 : lmax <= 8 ? 8 : 16; }
 
+#ifndef SKT_TILE_ONEBUF
+#define SKT_TILE_ONEBUF 1
+#endif
+#ifndef SKT_TILE_MINB
+#define SKT_TILE_MINB (SKT_TILE_ONEBUF ? 5 : 4)
+#endif
+
 template <typename IP, typename IX, typename TV, typename TOut, int kChunks>
-__global__ void __launch_bounds__(kTileWarps * 32, 4) csr_tile_kernel(
+__global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kernel(
     const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
     const IP *__restrict__ aip, const IX *__restrict__ aix, const TV *__restrict__ av, int d,
     int dp, int R, TOut *__restrict__ sa, int64_t ldsa) {
@@ -143,6 +150,78 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) csr_tile_kernel(
   int len1;
   row_desc(beg + R, w1, rs1, len1);
   uint32_t w2 = plan_word(beg + 2 * (int64_t)R);
+#if SKT_TILE_ONEBUF
+  // one register set: batch b is scattered first, then batch b+1's nonzeros
+  // are requested into the same registers and stay in flight while batch b
+  // is accumulated; the tile is cleared whole (no per-entry columns kept)
+  int slot = 0;
+  IX cc[16];
+  TV vv[16];
+  int g0 = publish(slot, beg, rs0, len0, w0);
+  __syncwarp();
+  load_sw(g0, descs + slot * 32, (int)((end - beg) < R ? (end - beg) : R), cc, vv);
+  for (int64_t k0 = beg; k0 < end; k0 += R) {
+    const int nrows = (int)((end - k0) < R ? (end - k0) : R);
+    const int4 *dcur = descs + slot * 32;
+    const int64_t k1 = k0 + R, k2 = k0 + 2 * (int64_t)R, k3 = k0 + 3 * (int64_t)R;
+    // ---- scatter batch b
+    if (g0 == 4)
+      store_rows<4>(dcur, tile, dp, lane, cc, vv);
+    else if (g0 == 8)
+      store_rows<8>(dcur, tile, dp, lane, cc, vv);
+    else
+      store_rows<16>(dcur, tile, dp, lane, cc, vv);
+    uint32_t longm = __ballot_sync(0xffffffffu, lane < nrows && len0 > g0);
+    while (longm) {  // rows longer than G: whole warp per row
+      const int r = __ffs(longm) - 1;
+      longm &= longm - 1;
+      const int4 ds = dcur[r];
+      const int64_t rs = (int64_t)(uint32_t)ds.x | ((int64_t)ds.y << 32);
+      for (int q = g0 + lane; q < ds.z; q += 32) {
+        const TV v = __ldg(av + rs + q);
+        tile[r * dp + (int)__ldg(aix + rs + q)] = ds.w ? -v : v;
+      }
+    }
+    // ---- batch b+1 in flight, descriptors of b+2, plan words of b+3
+    int g1 = 4;
+    if (k1 < end) {
+      g1 = publish(slot ^ 1, k1, rs1, len1, w1);
+      __syncwarp();
+      load_sw(g1, descs + (slot ^ 1) * 32, (int)((end - k1) < R ? (end - k1) : R), cc, vv);
+    }
+    int64_t rs2;
+    int len2;
+    row_desc(k2, w2, rs2, len2);
+    const uint32_t w3 = plan_word(k3);
+    __syncwarp();
+    // ---- accumulate batch b in row order
+    for (int r = 0; r < nrows; ++r) {
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = 64 * k + 2 * lane;
+        if (c < dp) {
+          const V2 x = *reinterpret_cast<const V2 *>(tile + r * dp + c);
+          acc[k][0] += (double)x.x;
+          acc[k][1] += (double)x.y;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- clear the batch's rows of the tile
+    {
+      uint4 *z = reinterpret_cast<uint4 *>(tile);
+      const int words = (int)(((size_t)nrows * dp * sizeof(TV) + 15) / 16);
+      for (int i = lane; i < words; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    g0 = g1;
+    len0 = len1;
+    rs1 = rs2;
+    len1 = len2;
+    w1 = w2;
+    w2 = w3;
+    slot ^= 1;
+  }
+#else
   int slot = 0;
   IX c0[16], c1[16];
   TV v0[16], v1[16];
@@ -224,6 +303,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 4) csr_tile_kernel(
     w2 = w3;
     slot ^= 1;
   }
+#endif
   TOut *o = sa + bucket * ldsa;
 #pragma unroll
   for (int k = 0; k < kChunks; ++k) {
