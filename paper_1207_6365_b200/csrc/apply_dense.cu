@@ -19,14 +19,17 @@ namespace skt {
 namespace {
 
 constexpr int kThreads = 256;
-// Tuned on config 3 (tools/dense_ceiling.py): software-pipelined gather
-// (batch k+1 in flight while batch k is accumulated), 4 rows per batch,
-// >= 3 resident blocks per SM.
+// Tuned on config 3 (tools/dense_ceiling.py, A/B builds on one box): one
+// batch of 4 rows in flight per warp (plan words one batch ahead), 60
+// registers, >= 4 resident blocks (32 warps) per SM -- 2% faster than the
+// software-pipelined gather (SKT_DENSE_PIPE=1: batch k+1 in flight while batch
+// k is accumulated, 80 registers, 24 warps per SM): more warps beat a deeper
+// per-warp pipeline, as in the CSR tile kernel.
 #ifndef SKT_DENSE_PIPE
-#define SKT_DENSE_PIPE 1
+#define SKT_DENSE_PIPE 0
 #endif
 #ifndef SKT_DENSE_MINB
-#define SKT_DENSE_MINB 3
+#define SKT_DENSE_MINB 4
 #endif
 
 template <typename T, int VEC>

@@ -290,6 +290,8 @@ class SparseEmbedding(SketchOperator):
         m = self.row_end - self.row_begin
         if not canonical or nnz is None or m == 0 or nnz > 8 * m or os.environ.get("SKT_CSR_KERNEL") in ("lane", "tile"):
             return 0
+        if os.environ.get("SKT_CSR_SHIFT"):  # A/B override
+            return int(os.environ["SKT_CSR_SHIFT"])
         shift, resident = 0, 148 * 32
         while shift < 8 and (self.output_dim >> shift) > resident and (2 << shift) * d * 8 <= 24 * 1024:
             shift += 1
