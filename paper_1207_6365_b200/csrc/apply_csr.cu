@@ -210,10 +210,17 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
   const size_t kSmemMax = 200 * 1024;
   int warps = (int)std::min<size_t>(kMaxWarps, kSmemMax / per_warp);
   if (warps < 1) {
-    // (5) too wide for shared memory: warp per bucket, fp64 accumulation in the output row
+    // (5) too wide for shared memory: fp64 accumulation in the output row, a
+    // block per bucket (few buckets) or a warp per bucket (SKT_CSR_ROWSEQ=warp)
     if (!canon) return fail(SKT_ENOTSUP, fn, "non-canonical CSR this wide is not supported");
     if (!std::is_same<TOut, double>::value)
       return fail(SKT_ENOTSUP, fn, "deterministic wide-d CSR writes fp64 SA (round on the host side)");
+    const char *rq = getenv("SKT_CSR_ROWSEQ");
+    if (!(rq && rq[0] == 'w')) {
+      SKT_LAUNCH((csr_rowseq_block_kernel<IP, IX, TV>), (unsigned)t, kRowseqThreads, 0, stream, pindptr, prow, t,
+                 (const IP *)aip, (const IX *)aix, (const TV *)av, d, (double *)sa, ldsa);
+      return check_launch(fn);
+    }
     const int64_t blocks = ((int64_t)t + 3) / 4;
     SKT_LAUNCH((csr_rowseq_kernel<IP, IX, TV, TOut>), (unsigned)blocks, 128, 0, stream, pindptr, prow, t,
                (const IP *)aip, (const IX *)aix, (const TV *)av, d, (double *)nullptr, (TOut *)sa, ldsa);

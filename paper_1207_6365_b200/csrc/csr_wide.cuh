@@ -56,6 +56,76 @@ __global__ void __launch_bounds__(256) csr_atomic_kernel(const int64_t *__restri
   }
 }
 
+// Deterministic wide-d kernel, one BLOCK per bucket (config 5: t = 400
+// buckets of ~655 rows, d = 262,144): the block walks the bucket's rows in
+// ascending order; a row's stored entries (distinct columns in canonical
+// CSR) are spread over all 256 threads, each adding s_i * v into the fp64
+// output row, and a block barrier separates consecutive rows -- so every
+// output element still receives its additions in ascending row order
+// (bit-identical).  The next row's indices / values are loaded before the
+// barrier; only the accumulator read-modify-write waits for it.  400 blocks x
+// 8 warps keep ~20x more loads in flight than a warp per bucket.
+constexpr int kRowseqThreads = 256;
+
+template <typename IP, typename IX, typename TV>
+__global__ void __launch_bounds__(kRowseqThreads) csr_rowseq_block_kernel(
+    const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
+    const IP *__restrict__ aip, const IX *__restrict__ aix, const TV *__restrict__ av, int64_t d,
+    double *__restrict__ sa, int64_t ldsa) {
+  constexpr int kPer = 4;  // entries per thread per step (rows up to 1024 entries in one pass)
+  const int64_t bucket = blockIdx.x;
+  if (bucket >= (int64_t)t) return;
+  double *acc = sa + bucket * ldsa;
+  for (int64_t c = threadIdx.x; c < d; c += kRowseqThreads) acc[c] = 0.0;
+  const int64_t beg = pindptr[bucket], end = pindptr[bucket + 1];
+  // row k's entries for this thread: positions rs + threadIdx.x + j * 256
+  auto load_row = [&](int64_t k, int64_t &rs, int64_t &re, double &sg) {
+    rs = re = 0;
+    sg = 1.0;
+    if (k < end) {
+      const uint32_t wrd = __ldg(prow + k);
+      const int64_t row = wrd & 0x7fffffffu;
+      sg = (wrd >> 31) ? -1.0 : 1.0;
+      rs = (int64_t)aip[row];
+      re = (int64_t)aip[row + 1];
+    }
+  };
+  int64_t rs, re;
+  double sg;
+  load_row(beg, rs, re, sg);
+  int64_t col[kPer];
+  double val[kPer];
+  auto load_entries = [&](int64_t b0, int64_t b1, double s) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int64_t p = b0 + threadIdx.x + (int64_t)j * kRowseqThreads;
+      col[j] = p < b1 ? (int64_t)__ldg(aix + p) : -1;
+      val[j] = p < b1 ? s * (double)__ldg(av + p) : 0.0;
+    }
+  };
+  load_entries(rs, rs + (re - rs < kPer * kRowseqThreads ? re - rs : kPer * kRowseqThreads), sg);
+  __syncthreads();  // zeroed row visible
+  for (int64_t k = beg; k < end; ++k) {
+    // entries of this row beyond the first kPer * 256 (long rows), in order
+    for (int64_t p0 = rs + kPer * kRowseqThreads; p0 < re; p0 += kRowseqThreads) {
+      const int64_t p = p0 + threadIdx.x;
+      if (p < re) acc[(int64_t)__ldg(aix + p)] += sg * (double)__ldg(av + p);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (col[j] >= 0) acc[col[j]] += val[j];
+    // the next row's entries go in flight before the barrier
+    int64_t rs2, re2;
+    double sg2;
+    load_row(k + 1, rs2, re2, sg2);
+    load_entries(rs2, rs2 + (re2 - rs2 < kPer * kRowseqThreads ? re2 - rs2 : kPer * kRowseqThreads), sg2);
+    rs = rs2;
+    re = re2;
+    sg = sg2;
+    __syncthreads();  // row k's additions before row k+1's
+  }
+}
+
 template <typename IP, typename IX, typename TV, typename TOut>
 __global__ void __launch_bounds__(128) csr_rowseq_kernel(const int64_t *__restrict__ pindptr,
                                                          const uint32_t *__restrict__ prow,

@@ -311,7 +311,11 @@ def test_apply_csr_wide_d(dtype, rng):
     """Config-5 shape (d too wide for on-chip accumulators): the deterministic
     wide kernel is bit-exact; fast mode (unordered atomics) is within rounding."""
     n, d, t = 6000, 60_000, 23
-    a = sp.csr_array(sp.random_array((n, d), density=0.002, rng=rng, format="csr"), dtype=dtype)
+    a = sp.random_array((n, d), density=0.002, rng=rng, format="csr").tolil()
+    for r in (3, 4, 2500):  # rows longer than one block pass (> 1024 stored entries)
+        cols = np.sort(rng.choice(d, size=3000, replace=False))
+        a[r, cols] = rng.standard_normal(3000)
+    a = sp.csr_array(a, dtype=dtype)
     op = SparseEmbedding(n, t, seed=5)
     h, s = O.hash_signs(n, t, 5)
     ref = O.np_apply_csr(h, s, t, a)
