@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "csr_group.cuh"
 #include "csr_lane.cuh"
+#include "csr_sweep.cuh"
 #include "csr_tile.cuh"
 #include "csr_wide.cuh"
 
@@ -155,6 +156,34 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
   }
   const int64_t gb = 1LL << shift;
   const bool short_rows = n > 0 && nnz <= 8 * n;  // mean row length <= 8
+  // (1a) tiled sweep over a bucket-group plan (rows of ~8+ nonzeros, narrow d,
+  // groups of 2 or 4 buckets)
+  if (canon && (shift == 1 || shift == 2) && !short_rows && d <= kTileMaxD) {
+    const int dp = (int)((d + 1) & ~1LL);
+    const int rmax = (int)std::min<int64_t>(32, tile_bytes<TV>() / ((int64_t)dp * sizeof(TV)));
+    int R = 16;
+    if (const char *e = getenv("SKT_SWEEP_R")) R = atoi(e) <= 16 ? 16 : 32;
+    if (R > rmax) R = 16;
+    const int64_t ngroups = (int64_t)((t - 1) >> shift) + 1;
+    const size_t smem = sweep_slice_bytes(R, dp, (int)sizeof(TV)) * kSweepWarps;
+    if (R <= rmax) {
+      const int64_t blocks = (ngroups + kSweepWarps - 1) / kSweepWarps;
+      const int chunks = (int)((d + 63) / 64);
+      typedef void (*KFn)(const int64_t *, const uint32_t *, const uint8_t *, int64_t, uint64_t, const IP *,
+                          const IX *, const TV *, int, int, TOut *, int64_t);
+#define SKT_SWEEP_PICK(RT, SH)                                                                    \
+  (chunks <= 1 ? (KFn)csr_sweep_kernel<IP, IX, TV, TOut, 1, RT, SH>                               \
+               : chunks <= 2 ? (KFn)csr_sweep_kernel<IP, IX, TV, TOut, 2, RT, SH>                 \
+                             : (KFn)csr_sweep_kernel<IP, IX, TV, TOut, 4, RT, SH>)
+      const KFn k = R == 16 ? (shift == 1 ? SKT_SWEEP_PICK(16, 1) : SKT_SWEEP_PICK(16, 2))
+                            : (shift == 1 ? SKT_SWEEP_PICK(32, 1) : SKT_SWEEP_PICK(32, 2));
+#undef SKT_SWEEP_PICK
+      SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+      SKT_LAUNCH(k, (unsigned)blocks, kSweepWarps * 32, smem, stream, pindptr, prow, blo, ngroups, t,
+                 (const IP *)aip, (const IX *)aix, (const TV *)av, (int)d, dp, (TOut *)sa, ldsa);
+      return check_launch(fn);
+    }
+  }
   // (1) grouped sweep over a bucket-group plan (short rows)
   const size_t group_acc = (size_t)gb * d * sizeof(double);
   if (canon && shift > 0 && group_acc <= 24 * 1024) {

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
       const int words = (int)(((size_t)nrows * dp * sizeof(TV) + 15) / 16);
       for (int i = lane; i < words; i += 32) z[i] = make_uint4(0, 0, 0, 0);
     }
+    __syncwarp();  // the clear lands before the next batch's scatter
     g0 = g1;
     len0 = len1;
     rs1 = rs2;

@@ -114,6 +114,16 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
       len = (int)((int64_t)aip[row + 1] - rs);
     }
   };
+  // raw indptr pair of a tile two ahead: converted one iteration later, so
+  // the loads stay in flight instead of stalling the warp right after issue
+  auto load_desc_raw = [&](int64_t tile, IP &b, IP &e) {
+    const int64_t row = tile * kTcRows + warp * 32 + lane;
+    b = e = (IP)0;
+    if (tile < ntiles && row < n) {
+      b = __ldg(aip + row);
+      e = __ldg(aip + row + 1);
+    }
+  };
   // nonzeros of a tile into registers: iteration i covers rows 4i + g, lanes
   // gl and gl + 8 of each row; the tail (nonzeros 16..79) of the warp's first
   // long row goes in flight too
@@ -162,6 +172,8 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
   load_desc(tile, rs_c, len_c);
   if (tile < ntiles) load_data(rs_c, len_c);
   load_desc(tile + gridDim.x, rs_n, len_n);
+  IP rb_2, re_2;
+  load_desc_raw(tile + 2 * (int64_t)gridDim.x, rb_2, re_2);
   for (; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * kTcRows;
     const uint32_t longm = __ballot_sync(0xffffffffu, len_c > NR);
@@ -286,7 +298,9 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
     if (tile + gridDim.x < ntiles) load_data(rs_n, len_n);
     rs_c = rs_n;
     len_c = len_n;
-    load_desc(tile + 2 * (int64_t)gridDim.x, rs_n, len_n);
+    rs_n = (int64_t)rb_2;
+    len_n = (int)((int64_t)re_2 - (int64_t)rb_2);
+    load_desc_raw(tile + 3 * (int64_t)gridDim.x, rb_2, re_2);
     // ---- wait for the accumulator
     asm volatile(
         "{ .reg .pred P; WAIT_%=: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra WAIT_%=; }" ::"r"(

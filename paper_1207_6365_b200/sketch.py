@@ -288,10 +288,12 @@ class SparseEmbedding(SketchOperator):
         one warp per group across the chip (148 SMs x 32 warps), group
         accumulators <= 24 KB.  Everything else sweeps the per-bucket plan."""
         m = self.row_end - self.row_begin
-        if not canonical or nnz is None or m == 0 or nnz > 8 * m or os.environ.get("SKT_CSR_KERNEL") in ("lane", "tile"):
+        if not canonical or nnz is None or m == 0 or os.environ.get("SKT_CSR_KERNEL") in ("lane", "tile"):
             return 0
         if os.environ.get("SKT_CSR_SHIFT"):  # A/B override
             return int(os.environ["SKT_CSR_SHIFT"])
+        if nnz > 8 * m:
+            return 0
         shift, resident = 0, 148 * 32
         while shift < 8 and (self.output_dim >> shift) > resident and (2 << shift) * d * 8 <= 24 * 1024:
             shift += 1

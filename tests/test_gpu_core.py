@@ -132,6 +132,31 @@ def test_apply_csr_bucket_lane_kernel(dtype, t, d, rng):
         op._apply_csr_device(*dev, d, torch.float64, canonical=False, shift=2)
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("d", [64, 100, 200])
+@pytest.mark.parametrize("tile_rows", ["16", "32"])
+def test_apply_csr_sweep_kernel(dtype, d, tile_rows, rng, monkeypatch):
+    """csr_sweep (bucket groups of 2 / 4 walked in ascending row order, rows
+    of ~16 nonzeros): bit-identical to the reference, incl. dense, empty and
+    rows longer than the prefetch width."""
+    monkeypatch.setenv("SKT_SWEEP_R", tile_rows)
+    n, t = 30_000, 1001
+    a = sp.csr_array(sp.random_array((n, d), density=16 / d, rng=rng, format="csr"), dtype=dtype)
+    a = a.tolil()
+    a[5, :] = rng.standard_normal(d)
+    a[6, :] = 0
+    a[29_999, ::3] = rng.standard_normal(len(range(0, d, 3)))
+    a = sp.csr_array(a, dtype=dtype)
+    op = SparseEmbedding(n, t, seed=d + 1)
+    h, s = O.hash_signs(n, t, d + 1)
+    ref = O.np_apply_csr(h, s, t, a)
+    dev = [torch.from_numpy(x).cuda() for x in (a.indptr, a.indices, a.data)]
+    for shift in (1, 2):
+        for out_dtype in (torch.float64, torch.float32):
+            got = op._apply_csr_device(*dev, d, out_dtype, canonical=True, shift=shift).cpu().numpy()
+            assert np.array_equal(got, ref.astype(got.dtype)), (shift, out_dtype)
+
+
 def test_host_views_match_reference_layout():
     op = make_sparse_embedding(9, 5, seed=1)
     h, s = O.hash_signs(9, 5, 1)

@@ -142,11 +142,26 @@ void run_csr(const char *name, int64_t n, int per, int dense_len) {
   // L2 flush buffer for inputs that fit in L2
   char *flush;
   cudaMalloc(&flush, 512 << 20);
-  for (int ordered = 0; ordered < 2; ++ordered) {
-    cudaMemcpy(dperm, perm.data(), n * 4, cudaMemcpyHostToDevice);
-    if (ordered) {
+  // windows: 1 = random permutation of all rows (the bucket-ordered plan);
+  // P > 1 = rows grouped into P contiguous row windows visited in order,
+  // random inside a window (a phased sweep); 0 = sequential rows
+  for (int windows : {1, 4, 8, 16, 32, 64, 0}) {
+    const int ordered = windows == 0;
+    if (windows == 1) {
+      cudaMemcpy(dperm, perm.data(), n * 4, cudaMemcpyHostToDevice);
+    } else {
       std::vector<uint32_t> id(n);
       for (int64_t i = 0; i < n; ++i) id[i] = (uint32_t)i;
+      if (windows > 1) {
+        for (int wi = 0; wi < windows; ++wi) {
+          const int64_t lo = n * wi / windows, hi = n * (wi + 1) / windows;
+          for (int64_t i = hi - 1; i > lo; --i) {
+            st = st * 6364136223846793005ULL + 1442695040888963407ULL;
+            const int64_t j = lo + (int64_t)((st >> 33) % (uint64_t)(i - lo + 1));
+            std::swap(id[i], id[j]);
+          }
+        }
+      }
       cudaMemcpy(dperm, id.data(), n * 4, cudaMemcpyHostToDevice);
     }
     for (int blocks : {148 * 6, 148 * 12, 148 * 16}) {
@@ -167,8 +182,8 @@ void run_csr(const char *name, int64_t n, int per, int dense_len) {
       }
       const float ms = total / 5;
       const double alg = nnz * (4.0 + sizeof(TV)) + (n + 1) * 4.0;
-      printf("csr gather (%s shape, %s rows, %d CTAs, L2 flushed): %.4f ms, %.0f GB/s algorithmic (%s)\n", name,
-             ordered ? "sequential" : "random", blocks, ms, alg / (ms * 1e-3) / 1e9,
+      printf("csr gather (%s shape, %s rows, windows %d, %d CTAs, L2 flushed): %.4f ms, %.0f GB/s algorithmic (%s)\n", name,
+             ordered ? "sequential" : "random", windows, blocks, ms, alg / (ms * 1e-3) / 1e9,
              cudaGetErrorString(cudaGetLastError()));
     }
   }
@@ -202,9 +217,10 @@ void run(const float *p, int64_t nfloats, float *out, int align) {
          nseg * kSeg * 4.0 / (ms * 1e-3) / 1e9, ms, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+int main(int argc, char **argv) {
   run_csr<16, float>("config-4", 4194304, 16, 64);
   run_csr<8, double>("config-2", 1000000, 5, 0);
+  if (argc > 1) return 0;  // CSR patterns only
   const int64_t nfloats = (int64_t)2 << 30;  // 8 GB
   float *p, *out;
   cudaMalloc(&p, nfloats * 4);
