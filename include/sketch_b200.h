@@ -175,6 +175,51 @@ skt_status skt_residual_csr(int64_t n, int64_t d, const void *a_indptr, skt_ityp
                             skt_dtype b_dtype, int64_t ldb, double *out_sq, void *ws,
                             size_t ws_bytes, void *stream);
 
+/* ---- passes of the preconditioned iterations and the rank-k residual ----- */
+/* SURVEY §8f rank 2, the passes over original data after the sketch.  M is
+ * the n x r row-major fp64 product A R (regress.py:203, r <= 256); y, p are
+ * r-vectors, b, q, rvec n-vectors (one right-hand-side column per call), all
+ * fp64 on the device.  Reductions go through per-block partials in the
+ * workspace (skt_lsq_workspace) and one fixed-order pass: deterministic.
+ *  skt_lsq_residual_grad: *res2 = ||b - M y||^2, g = M^T (b - M y) (g may be
+ *    NULL) -- Richardson's step y + M^T (b - M y) (regress.py:237-241) and the
+ *    residual _iterate records (regress.py:209), one read of M.
+ *  skt_lsq_matvec_norm: q = M p, *qq = ||q||^2 -- CGNR's mp and denom
+ *    (regress.py:274-275).
+ *  skt_lsq_update_grad: rvec <- rvec - q * alpha (product rounded, as numpy),
+ *    z = M^T rvec, *res2 = ||M y - b||^2 -- CGNR's r, z (regress.py:278-279)
+ *    and the residual of the new iterate, one read of M.
+ *  skt_spmm_csr: Y = A X (n x k, ldy), A CSR, X d x k fp64 -- M = A R for a
+ *    sparse A (regress.py:203).
+ *  skt_gram_cross_csr / _dense: out2[0] = sum_i <A_i Mw, L_i>, out2[1] =
+ *    ||A||_F^2 for Mw = W diag(d) (ncols x k, k <= 64) and L (n x k): the
+ *    Gram-identity residual ||A - L D W^T||^2 = out2[1] - 2 out2[0] + sum d^2
+ *    (lowrank.py:100-108), one read of A.  Workspace: skt_lsq_workspace(0). */
+skt_status skt_lsq_workspace(int64_t r, size_t *bytes);
+skt_status skt_lsq_residual_grad(int64_t n, int64_t r, const double *m, int64_t ldm, const double *y,
+                                 const double *b, int64_t ldb, double *g, double *res2, void *ws,
+                                 size_t ws_bytes, void *stream);
+skt_status skt_lsq_matvec_norm(int64_t n, int64_t r, const double *m, int64_t ldm, const double *p,
+                               double *q, int64_t ldq, double *qq, void *ws, size_t ws_bytes,
+                               void *stream);
+skt_status skt_lsq_update_grad(int64_t n, int64_t r, const double *m, int64_t ldm, const double *q,
+                               int64_t ldq, double alpha, double *rvec, int64_t ldr, const double *y,
+                               const double *b, int64_t ldb, double *z, double *res2, void *ws,
+                               size_t ws_bytes, void *stream);
+skt_status skt_spmm_csr(int64_t n, int64_t d, const void *a_indptr, skt_itype indptr_type,
+                        const void *a_indices, skt_itype index_type, const void *a_vals,
+                        skt_dtype val_dtype, int64_t nnz, const double *x, int64_t k, double *y,
+                        int64_t ldy, void *stream);
+skt_status skt_gram_cross_csr(int64_t n, int64_t ncols, const void *a_indptr, skt_itype indptr_type,
+                              const void *a_indices, skt_itype index_type, const void *a_vals,
+                              skt_dtype val_dtype, const double *mw, int64_t ldm, int64_t k,
+                              const double *l, int64_t ldl, double *out2, void *ws, size_t ws_bytes,
+                              void *stream);
+skt_status skt_gram_cross_dense(int64_t n, int64_t ncols, const void *a, skt_dtype a_dtype,
+                                int64_t lda, const double *mw, int64_t ldm, int64_t k,
+                                const double *l, int64_t ldl, double *out2, void *ws,
+                                size_t ws_bytes, void *stream);
+
 /* ---- SRHT of a tall fp64 matrix ---------------------------------------- */
 /* Replaces SrhtOperator.apply (sketch.py:284-291) on device data: rows of A
  * (n x d, lda) zero-padded to n_pad = 2^ceil(log2 n), multiplied by sign[i]

@@ -22,6 +22,7 @@ from .sketch import (
     to_descriptor,
 )
 from .generalized import GeneralizedSparseEmbedding, generalized_dims, make_generalized_sparse_embedding
+from .precond import Preconditioner, SolverError, cgnr_solve, precondition, richardson_solve
 from .shim import install, uninstall
 
 __version__ = "0.1.0"

@@ -6,6 +6,9 @@ CountSketch path and its callers read are kept; default_sparse_dim
 SPARSE_DIM_C = 1.0
 SPARSE_DIM_FLOOR = 4
 
+# SRHT rows t = C (sqrt r + sqrt log n)^2 log(r + 1) / eps^2 (sketch.py:83-94)
+SRHT_DIM_C = 1.5
+
 # leverage.py:100-107 and :87 (JL probe width)
 LEVERAGE_F_C = 40.0
 LEVERAGE_JL_C = 16.0

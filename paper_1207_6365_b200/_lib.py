@@ -45,6 +45,13 @@ EXPORTS = (
     "skt_residual_workspace",
     "skt_residual_dense",
     "skt_residual_csr",
+    "skt_lsq_workspace",
+    "skt_lsq_residual_grad",
+    "skt_lsq_matvec_norm",
+    "skt_lsq_update_grad",
+    "skt_spmm_csr",
+    "skt_gram_cross_csr",
+    "skt_gram_cross_dense",
     "skt_srht_workspace",
     "skt_srht_apply",
     "skt_gse_buckets",
@@ -132,6 +139,13 @@ def lib() -> ctypes.CDLL:
         "skt_residual_workspace": ([ctypes.POINTER(sz)], i32),
         "skt_residual_dense": ([i64, i64, P, i32, i64, P, i64, P, i32, i64, P, P, sz, P], i32),
         "skt_residual_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, i64, P, P, sz, P], i32),
+        "skt_lsq_workspace": ([i64, ctypes.POINTER(sz)], i32),
+        "skt_lsq_residual_grad": ([i64, i64, P, i64, P, P, i64, P, P, P, sz, P], i32),
+        "skt_lsq_matvec_norm": ([i64, i64, P, i64, P, P, i64, P, P, sz, P], i32),
+        "skt_lsq_update_grad": ([i64, i64, P, i64, P, i64, ctypes.c_double, P, i64, P, P, i64, P, P, P, sz, P], i32),
+        "skt_spmm_csr": ([i64, i64, P, i32, P, i32, P, i32, i64, P, i64, P, i64, P], i32),
+        "skt_gram_cross_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, i64, P, i64, P, P, sz, P], i32),
+        "skt_gram_cross_dense": ([i64, i64, P, i32, i64, P, i64, i64, P, i64, P, P, sz, P], i32),
         "skt_srht_workspace": ([i64, i64, ctypes.POINTER(sz)], i32),
         "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),
         "skt_gse_buckets": ([P, P, i64, i32, u32, u64, P, P], i32),

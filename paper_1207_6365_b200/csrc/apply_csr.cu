@@ -158,7 +158,8 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
   const bool short_rows = n > 0 && nnz <= 8 * n;  // mean row length <= 8
   // (1a) tiled sweep over a bucket-group plan (rows of ~8+ nonzeros, narrow d,
   // groups of 2 or 4 buckets)
-  if (canon && (shift == 1 || shift == 2) && !short_rows && d <= kTileMaxD) {
+  static const bool sweep_short = getenv("SKT_SWEEP_SHORT") != nullptr;  // A/B: sweep short rows too
+  if (canon && (shift == 1 || shift == 2) && (!short_rows || sweep_short) && d <= kTileMaxD) {
     const int dp = (int)((d + 1) & ~1LL);
     const int rmax = (int)std::min<int64_t>(32, tile_bytes<TV>() / ((int64_t)dp * sizeof(TV)));
     int R = 16;

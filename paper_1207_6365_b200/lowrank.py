@@ -106,13 +106,17 @@ def _frobenius_norm(a) -> float:
 
 
 def _residual_norm(a, l, d, w) -> float:
-    """lowrank.py:100-108 (dense below 4M entries, Gram identity above)."""
+    """lowrank.py:100-108 (dense below 4M entries, Gram identity above).  The
+    Gram branch's two passes over A (a @ (w d) with the row dot against L, and
+    ||A||_F^2) are one fused GPU pass (skt_gram_cross_*, precond.gram_residual_sq)."""
     n, n_cols = a.shape
     if n * n_cols <= DENSE_RESIDUAL_LIMIT:
         dense = a.toarray() if sp.issparse(a) else a
         return float(np.linalg.norm(dense - (l * d) @ w.T, "fro"))
-    cross = np.einsum("ij,ij->", np.asarray(a @ (w * d)), l)
-    val = _frobenius_norm(a) ** 2 - 2.0 * cross + float(np.sum(d**2))
+    from .precond import gram_residual_sq  # noqa: PLC0415
+
+    cross, fro2 = gram_residual_sq(a, l, d, w)
+    val = fro2 - 2.0 * cross + float(np.sum(d**2))
     return float(math.sqrt(max(val, 0.0)))
 
 

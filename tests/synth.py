@@ -92,3 +92,45 @@ def lev_case():
     a = sp.csr_array(a)
     a.sort_indices()
     return a, 2_000, 32, 7
+
+
+def csr_matvec_fixed_order(a: sp.csr_array, x: np.ndarray, per_row: int) -> np.ndarray:
+    """A @ x for a CSR with exactly `per_row` entries per row, summed slot by
+    slot with elementwise ufuncs (bit-identical on every host)."""
+    v = a.data.reshape(-1, per_row) * x[a.indices, 0].reshape(-1, per_row)
+    acc = v[:, 0]
+    for j in range(1, per_row):
+        acc = acc + v[:, j]
+    return acc.reshape(-1, 1)
+
+
+def precond_cases():
+    """Inputs of the preconditioned-iteration cases (regress.py:159-283):
+    name -> (A, b, eps0, seed).  Ill-conditioned columns (scaled 1 .. 1e3),
+    a two-column right-hand side, a rank-deficient A, a CSR A."""
+    rng = np.random.default_rng(41)
+    n, d = 20_000, 12
+    a = rng.standard_normal((n, d)) * (10.0 ** np.linspace(0.0, 3.0, d))
+    x = rng.standard_normal((d, 1))
+    b = matvec_fixed_order(a, x) + 0.01 * rng.standard_normal((n, 1))
+    b2 = np.hstack([b, 0.5 * b + rng.standard_normal((n, 1))])
+    a_def = a.copy()
+    a_def[:, 5] = 2.0 * a_def[:, 2]
+    s = csr_fixed_nnz(rng, 50_000, 20, 6)
+    xs = rng.standard_normal((20, 1))
+    bs = csr_matvec_fixed_order(s, xs, 6) + 0.01 * rng.standard_normal((50_000, 1))
+    return {
+        "dense": (a, b, 0.5, 3),
+        "dense_2col": (a, b2, 0.5, 4),
+        "rank_deficient": (a_def, b, 0.5, 5),
+        "csr": (s, bs, 0.5, 6),
+    }
+
+
+def gram_cases():
+    """Inputs of the rank-k Gram residual (lowrank.py:100-108) above the 4M
+    entry limit: name -> A (CSR 3000 x 2000 at 1%, dense 2100 x 2000)."""
+    rng = np.random.default_rng(43)
+    s = sp.csr_array(sp.random_array((3000, 2000), density=0.01, rng=rng, format="csr"))
+    dense = rng.standard_normal((2100, 2000))
+    return {"csr": s, "dense": dense}
