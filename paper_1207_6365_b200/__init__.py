@@ -23,6 +23,7 @@ from .sketch import (
 )
 from .generalized import GeneralizedSparseEmbedding, generalized_dims, make_generalized_sparse_embedding
 from .precond import Preconditioner, SolverError, cgnr_solve, precondition, richardson_solve
+from .solvers import SrhtOperator, lawson_hanson_nnls, nonneg_regression, srht_or_identity
 from .shim import install, uninstall
 
 __version__ = "0.1.0"

@@ -1,16 +1,16 @@
 """Rank-k approximation with the sketches on the GPU -- mirror of the
-reference's ``low_rank_approx`` (lowrank.py:111-222) for the case BASELINE
-config 5 exercises: explicit sparse-embedding sketches ``r_op`` (column sketch
-of the row space, step 1) and ``s_op`` (affine row sketch, step 2).
+reference's ``low_rank_approx`` (lowrank.py:111-222): the default
+"srht_compose" strategy (each sketch an SRHT composed with a sparse
+embedding) and explicit sparse-embedding sketches ``r_op`` / ``s_op`` (BASELINE
+config 5).
 
-GPU: the column sketch Y = A R^T (transpose-free kernel, sketch.py:445-448),
-S U and S A (K3 / K4).  Host: the thin SVDs / truncations of the small
-sketched problems and the Gram-identity residual -- the reference's own
-numpy/scipy code path, so the factors match to LAPACK rounding.  The default
-strategies compose SRHT / leverage samplers (other sketch families, outside
-this package's scope); without explicit sketches they are delegated to the
-reference package when it is importable.
-"""
+GPU: the column sketch Y = A R^T (transpose-free kernel, sketch.py:445-448,
+then the SRHT of the small sketch), S U and S A (K3 / K4 + SRHT), and the
+Gram-identity residual (one fused pass over A, csrc/lsq.cu).  Host: the thin
+SVDs / truncations of the small sketched problems -- the reference's own
+numpy calls, so the factors match to LAPACK rounding.  "leverage_sample"
+(leverage-score row samplers, another sketch family) is delegated to the
+reference package when it is importable."""
 
 from __future__ import annotations
 
@@ -21,8 +21,9 @@ import numpy as np
 import scipy.sparse as sp
 import torch
 
-from .sketch import apply_right, check_count, check_eps
-from .solvers import as_matrix
+from .sketch import ComposedSketch, apply_right, check_count, check_eps, default_sparse_dim
+from .sketch import sparse_embedding_or_identity
+from .solvers import as_matrix, srht_or_identity
 
 RANK_REL_TOL = 1e-10
 DENSE_RESIDUAL_LIMIT = 4_000_000  # lowrank.py:41
@@ -120,16 +121,25 @@ def _residual_norm(a, l, d, w) -> float:
     return float(math.sqrt(max(val, 0.0)))
 
 
+STRATEGIES = ("srht_compose", "leverage_sample")  # lowrank.py:39
+
+
 def low_rank_approx(a, k: int, eps: float, seed: int = 0, strategy: str = "srht_compose",
                     t_r: int | None = None, r_op=None, s_op=None, **kw) -> LowRankResult:
-    """lowrank.py:111-222 with explicit sketches; see module docstring."""
-    if r_op is None or s_op is None:
+    """lowrank.py:111-222.  The default strategy ("srht_compose": SRHT o sparse
+    embedding for both sketches) and explicit sparse-embedding sketches run
+    here with every sketch on the GPU; "leverage_sample" (leverage-score row
+    samplers, another sketch family) is handed to the reference package when
+    it is importable."""
+    if strategy not in STRATEGIES:
+        raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
+    if strategy != "srht_compose" and (r_op is None or s_op is None):
         try:
             from sketchnla import lowrank as _ref  # noqa: PLC0415
         except ImportError:
             raise ValueError(
-                "low_rank_approx without explicit r_op/s_op needs SRHT/leverage sketches "
-                "(outside this package); pass sparse-embedding r_op and s_op"
+                "low_rank_approx(strategy='leverage_sample') samples rows by leverage scores "
+                "(outside this package); use 'srht_compose' or pass r_op and s_op"
             ) from None
         return _ref.low_rank_approx(a, k, eps, seed=seed, strategy=strategy, t_r=t_r, r_op=r_op,
                                     s_op=s_op, **kw)
@@ -140,10 +150,22 @@ def low_rank_approx(a, k: int, eps: float, seed: int = 0, strategy: str = "srht_
         raise ValueError(f"k={k} out of range for shape {a.shape}")
     eps = check_eps(eps)
     dims_t_r, v, v_prime = sketch_dims_lowrank(k, eps)
-    t_r = dims_t_r if t_r is None else check_count(t_r, "t_r")
+    if t_r is None:
+        t_r = dims_t_r
+    else:
+        t_r = check_count(t_r, "t_r")
+        v, v_prime = _affine_dims(t_r, eps)
 
     def stream(j):
         return int(np.random.SeedSequence(int(seed), spawn_key=(7, j)).generate_state(1)[0])
+
+    if r_op is None:  # srht_compose (lowrank.py:154-157)
+        t_hat = min(max(2 * t_r, default_sparse_dim(k, eps)), n_cols)
+        inner = sparse_embedding_or_identity(n_cols, t_hat, stream(1))
+        r_op = ComposedSketch(srht_or_identity(inner.output_dim, t_r, stream(0)), inner)
+    if s_op is None:  # srht_compose (lowrank.py:180-184)
+        inner = sparse_embedding_or_identity(n, min(v, n), stream(3))
+        s_op = ComposedSketch(srht_or_identity(inner.output_dim, v_prime, stream(2)), inner)
 
     # step 1: row-space sketch Y = A R^T on the GPU, orthonormal basis on the host
     y = apply_right(a, r_op)
@@ -153,8 +175,8 @@ def low_rank_approx(a, k: int, eps: float, seed: int = 0, strategy: str = "srht_
                                  w=_pad_orthonormal(np.zeros((n_cols, 0)), k, stream(10)), k=k)
         return LowRankResult(factors, _frobenius_norm(a), 1.0, t_r, 0, strategy, int(seed))
     # step 2: affine sketch of (U, A) on the GPU
-    su = s_op.apply(u)
-    sa = s_op.apply(a)
+    su = np.asarray(s_op.apply(u))
+    sa = np.asarray(s_op.apply(a))
     t_s = s_op.output_dim
     cond_su = _condition_number(su)
     # steps 3-5 on the host (small)

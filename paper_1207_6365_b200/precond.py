@@ -33,20 +33,21 @@ import numpy as np
 import scipy.sparse as sp
 import torch
 
-from . import _constants as C
 from . import _lib
 from ._lib import check
-from .sketch import _ITYPE, _TORCH_TO_SKT, _ptr, _stream_ptr, check_count, check_eps, default_sparse_dim
+from .sketch import _ITYPE, _TORCH_TO_SKT, _ptr, _stream_ptr, check_eps, default_sparse_dim
 from .sketch import sparse_embedding_or_identity
-from .solvers import RegressionSolution, as_dense, as_matrix, pivoted_qr_rank, residual_fro, srht_apply
-
-
-class SolverError(RuntimeError):
-    """regress.py:36-41: an iterative solve that failed; ``best`` is the last iterate."""
-
-    def __init__(self, message, best=None):
-        super().__init__(message)
-        self.best = best
+from .solvers import (  # noqa: F401  (SolverError re-exported)
+    RegressionSolution,
+    SolverError,
+    _seed_stream,
+    as_dense,
+    as_matrix,
+    default_srht_dim,
+    pivoted_qr_rank,
+    residual_fro,
+    srht_apply,
+)
 
 
 @dataclass(frozen=True)
@@ -58,20 +59,6 @@ class Preconditioner:
     seed: int
     rank: int
     sketch_dim: int
-
-
-def _seed_stream(seed: int, *key: int) -> int:
-    """regress.py:76-77."""
-    return int(np.random.SeedSequence(int(seed), spawn_key=key).generate_state(1)[0])
-
-
-def default_srht_dim(r: int, eps: float, n: int) -> int:
-    """sketch.py:83-94."""
-    r = check_count(r, "r")
-    n = check_count(n, "n")
-    eps = check_eps(eps)
-    t = C.SRHT_DIM_C * (math.sqrt(r) + math.sqrt(math.log(max(n, 2)))) ** 2 * math.log(r + 1.0) / eps**2
-    return max(r + 1, math.ceil(t))
 
 
 def precondition(a, eps0: float, seed: int = 0) -> Preconditioner:

@@ -21,15 +21,19 @@ import scipy.linalg
 import scipy.sparse as sp
 import torch
 
+from . import _constants as _C
 from . import _lib
 from ._lib import check
 from .sketch import (
+    ComposedSketch,
+    IdentityOperator,
     SparseEmbedding,
     _ITYPE,
     _TORCH_TO_SKT,
     _host,
     _ptr,
     _stream_ptr,
+    check_count,
     check_eps,
     default_sparse_dim,
     pcg64_state,
@@ -279,13 +283,33 @@ def leverage_scores_sketched(a, m: int, k: int, seed: int, rep: int = 0) -> Leve
     return LeverageRun(scores, rank, sa, probe)
 
 
-def srht_apply(a, t: int, seed: int, device=None):
+def _srht_draws(n_pad: int, seed: int, device):
+    """The SRHT's sign vector (stream (2, 0) .choice over n_pad) and its row
+    draws (stream (2, 1) .integers(0, n_pad)), one K1 call: bucket stream
+    (2, 1) with t = n_pad, sign stream (2, 0) -- n_pad row draws; an operator
+    with t samples uses the first t (sketch.py:276-281)."""
+    L = _lib.lib()
+    hs, ss = pcg64_state(seed, (2, 1)), pcg64_state(seed, (2, 0))
+    rows = torch.empty(n_pad, dtype=torch.int32, device=device)
+    sign = torch.empty(n_pad, dtype=torch.int8, device=device)
+    kb = ctypes.c_size_t()
+    check(L.skt_hash_signs_workspace(n_pad, n_pad, ctypes.byref(kb)))
+    kws = torch.empty(max(kb.value, 8), dtype=torch.uint8, device=device)
+    with torch.cuda.device(device):
+        check(L.skt_hash_signs(ctypes.byref(hs), ctypes.byref(ss), 0, n_pad, n_pad, _ptr(rows), _ptr(sign),
+                               _ptr(kws), kb.value, _stream_ptr(device)))
+        torch.cuda.current_stream(device).synchronize()
+    return rows, sign
+
+
+def srht_apply(a, t: int, seed: int, device=None, all_rows: bool = False):
     """SrhtOperator(n, t, seed).apply(a) (sketch.py:255-291) on the GPU
     (skt_srht_apply: sign flip + padding, the reference's _fwht butterflies
     stage by stage, sampling + scaling), bit-identical to the reference.  The
     sign vector and the sampled rows are the reference's streams (2, 0) and
-    (2, 1) of SeedSequence(seed), drawn on the GPU by K1.  ``a``: numpy or
-    torch (n x d or n); returns the same kind (torch on ``a``'s device)."""
+    (2, 1) of SeedSequence(seed), drawn on the GPU by K1 (``all_rows``: every
+    padded row in order, t = n_pad).  ``a``: numpy or torch (n x d or n);
+    returns the same kind (torch on ``a``'s device)."""
     if device is None:
         device = a.device if isinstance(a, torch.Tensor) and a.is_cuda else torch.device(
             "cuda", torch.cuda.current_device())
@@ -298,24 +322,19 @@ def srht_apply(a, t: int, seed: int, device=None):
     if n < 1 or t < 1:
         raise ValueError("n and t must be >= 1")
     n_pad = 1 << (n - 1).bit_length()
+    if all_rows:
+        t = n_pad
     if t > n_pad:
         raise ValueError(f"t={t} exceeds padded dimension {n_pad}")
 
     scale = math.sqrt(n_pad / t) / math.sqrt(n_pad)
     out = torch.empty((t, d), dtype=torch.float64, device=device)
     L = _lib.lib()
+    rows, sign = _srht_draws(n_pad, seed, device)
+    if all_rows:
+        rows = torch.arange(n_pad, dtype=torch.int32, device=device)
     with torch.cuda.device(device):
         stream = _stream_ptr(device)
-        # sign = stream (2, 0) .choice over n_pad, rows = stream (2, 1)
-        # .integers(0, n_pad, t): one K1 call (bucket stream (2, 1), t = n_pad)
-        hs, ss = pcg64_state(seed, (2, 1)), pcg64_state(seed, (2, 0))
-        rows = torch.empty(n_pad, dtype=torch.int32, device=device)
-        sign = torch.empty(n_pad, dtype=torch.int8, device=device)
-        kb = ctypes.c_size_t()
-        check(L.skt_hash_signs_workspace(n_pad, n_pad, ctypes.byref(kb)))
-        kws = torch.empty(max(kb.value, 8), dtype=torch.uint8, device=device)
-        check(L.skt_hash_signs(ctypes.byref(hs), ctypes.byref(ss), 0, n_pad, n_pad, _ptr(rows), _ptr(sign),
-                               _ptr(kws), kb.value, stream))
         wsb = ctypes.c_size_t()
         check(L.skt_srht_workspace(n, d, ctypes.byref(wsb)))
         ws = torch.empty(max(wsb.value, 8), dtype=torch.uint8, device=device)
@@ -325,6 +344,166 @@ def srht_apply(a, t: int, seed: int, device=None):
     if one_d:
         out = out.reshape(-1)
     return _host(out).numpy() if host else out
+
+
+class SrhtOperator:
+    """sketch.py:255-302: subsampled randomized Hadamard transform, applied on
+    the GPU (srht_apply).  ``sign`` / ``sampled_rows`` are host views of the
+    K1 draws (the reference's arrays, bit for bit)."""
+
+    family = "srht"
+
+    def __init__(self, n: int, t: int, seed: int, all_rows: bool = False, device=None):
+        self.input_dim = check_count(n, "n")
+        self.n_pad = 1 << (self.input_dim - 1).bit_length()
+        self.seed = int(seed)
+        self.all_rows = bool(all_rows)
+        if all_rows:
+            t = self.n_pad
+        self.output_dim = check_count(t, "t")
+        if self.output_dim > self.n_pad:
+            raise ValueError(f"t={t} exceeds padded dimension {self.n_pad}")
+        self.scale = math.sqrt(self.n_pad / self.output_dim) / math.sqrt(self.n_pad)
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._views = None
+
+    def _draws(self):
+        if self._views is None:
+            rows, sign = _srht_draws(self.n_pad, self.seed, self.device)
+            picks = np.arange(self.n_pad) if self.all_rows else rows[: self.output_dim].cpu().numpy().astype(np.int64)
+            self._views = (sign.cpu().numpy().astype(np.float64), picks)
+        return self._views
+
+    @property
+    def sign(self) -> np.ndarray:
+        return self._draws()[0]
+
+    @property
+    def sampled_rows(self) -> np.ndarray:
+        return self._draws()[1]
+
+    def apply(self, a):
+        if a.shape[0] != self.input_dim:
+            raise ValueError(f"operator expects {self.input_dim} rows, got {a.shape[0]}")
+        if isinstance(a, torch.Tensor):
+            x = a.to_dense() if a.layout != torch.strided else a
+            return srht_apply(x.to(self.device), self.output_dim, self.seed, self.device, self.all_rows)
+        return srht_apply(as_dense(a), self.output_dim, self.seed, self.device, self.all_rows)
+
+    def dense(self) -> np.ndarray:
+        return self.apply(np.eye(self.input_dim))
+
+    def descriptor(self) -> dict:
+        return {"family": self.family, "n": self.input_dim, "t": self.output_dim, "seed": self.seed,
+                "all_rows": self.all_rows}
+
+
+def default_srht_dim(r: int, eps: float, n: int) -> int:
+    """sketch.py:83-94."""
+    r = check_count(r, "r")
+    n = check_count(n, "n")
+    eps = check_eps(eps)
+    t = _C.SRHT_DIM_C * (math.sqrt(r) + math.sqrt(math.log(max(n, 2)))) ** 2 * math.log(r + 1.0) / eps**2
+    return max(r + 1, math.ceil(t))
+
+
+def srht_or_identity(n: int, t: int, seed: int):
+    """sketch.py:429-433."""
+    if t >= n:
+        return IdentityOperator(n)
+    return SrhtOperator(n, t, seed)
+
+
+# ---------------------------------------------------------------------------
+# nonnegative regression (regress.py:288-370)
+# ---------------------------------------------------------------------------
+class SolverError(RuntimeError):
+    """regress.py:36-41: an iterative / active-set solve that failed; ``best``
+    is the last iterate."""
+
+    def __init__(self, message, best=None):
+        super().__init__(message)
+        self.best = best
+
+
+def lawson_hanson_nnls(m, y, dual_tol: float = 1e-8, max_passes: int | None = None) -> np.ndarray:
+    """Lawson-Hanson active-set NNLS, min ||m x - y|| s.t. x >= 0 (regress.py:
+    288-327): add the inactive coordinate with the largest dual value, solve
+    least squares on the passive set, and step back to the feasible boundary
+    while the passive solution has non-positive entries.  Stops when every
+    inactive dual value is <= dual_tol * max(max |w_0|, 1); raises SolverError
+    after max_passes (default 10 d + 50) additions.  Host code on the small
+    sketched problem, as in the reference."""
+    m = as_dense(m)
+    y = np.asarray(y, dtype=np.float64).ravel()
+    d = m.shape[1]
+    cap = 10 * d + 50 if max_passes is None else max_passes
+    x = np.zeros(d)
+    passive = np.zeros(d, dtype=bool)
+    w = m.T @ (y - m @ x)
+    scale = max(np.abs(w).max(initial=0.0), 1.0)
+    added = 0
+    while True:
+        free = ~passive
+        if not free.any() or w[free].max(initial=-np.inf) <= dual_tol * scale:
+            return x
+        added += 1
+        if added > cap:
+            raise SolverError("NNLS did not converge within the pass cap", best=x)
+        candidates = np.flatnonzero(free)
+        passive[candidates[np.argmax(w[free])]] = True
+        while True:
+            cols = np.flatnonzero(passive)
+            z = np.zeros(d)
+            z[cols] = np.linalg.lstsq(m[:, cols], y, rcond=None)[0]
+            if z[cols].min(initial=np.inf) > 0:
+                x = z
+                break
+            blocking = cols[z[cols] <= 0]  # passive coordinates the full step would push to <= 0
+            step = np.min(x[blocking] / np.maximum(x[blocking] - z[blocking], 1e-300))
+            x = x + step * (z - x)
+            passive &= x > 1e-14
+        w = m.T @ (y - m @ x)
+
+
+def nonneg_regression(a, b, eps: float, seed: int = 0, operator=None) -> RegressionSolution:
+    """regress.py:330-370: min_{X >= 0} ||A X - B|| on an affine-embedding
+    sketch -- SRHT o sparse embedding, each at eps / 3 -- applied on the GPU
+    (K1-K4, then the SRHT of the small sketch), Lawson-Hanson per column on
+    the host, the residual on the original data by the fused GPU pass."""
+    a = as_matrix(a)
+    b = as_dense(b)
+    if a.shape[0] != b.shape[0]:
+        raise ValueError(f"operands must have the same number of rows: {a.shape[0]} vs {b.shape[0]}")
+    eps = check_eps(eps)
+    if operator is None:
+        joint = a.shape[1] + b.shape[1]
+        n = a.shape[0]
+        t1 = min(default_sparse_dim(joint, eps / 3), n)
+        inner = sparse_embedding_or_identity(n, t1, _seed_stream(seed, 0))
+        t2 = default_srht_dim(joint, eps / 3, inner.output_dim)
+        operator = ComposedSketch(srht_or_identity(inner.output_dim, t2, _seed_stream(seed, 1)), inner)
+    sa = np.asarray(_host_array(operator.apply(a)))
+    sb = np.asarray(_host_array(operator.apply(b)))
+    x = np.column_stack([lawson_hanson_nnls(sa, sb[:, j]) for j in range(sb.shape[1])])
+    device = getattr(getattr(operator, "inner", operator), "device", None) or torch.device(
+        "cuda", torch.cuda.current_device())
+    return RegressionSolution(
+        x=x,
+        residual_norm=_residual_fro_gpu(a, x, b, device),
+        method="nnls",
+        sketch_dim=operator.output_dim,
+        seed=int(seed),
+    )
+
+
+def _host_array(x):
+    return _host(x).numpy() if isinstance(x, torch.Tensor) else x
+
+
+def _seed_stream(seed: int, *key: int) -> int:
+    """regress.py:76-77."""
+    return int(np.random.SeedSequence(int(seed), spawn_key=key).generate_state(1)[0])
 
 
 @dataclass(frozen=True)

@@ -134,3 +134,32 @@ def gram_cases():
     s = sp.csr_array(sp.random_array((3000, 2000), density=0.01, rng=rng, format="csr"))
     dense = rng.standard_normal((2100, 2000))
     return {"csr": s, "dense": dense}
+
+
+def nnls_cases():
+    """Inputs of nonneg_regression (regress.py:330-370): name -> (A, b, eps, seed)."""
+    rng = np.random.default_rng(47)
+    n, d = 30_000, 8
+    a = rng.standard_normal((n, d))
+    x = np.array([[1.5], [-0.7], [0.3], [2.0], [-1.2], [0.0], [0.8], [-0.1]])
+    b = matvec_fixed_order(a, x) + 0.05 * rng.standard_normal((n, 1))
+    b2 = np.hstack([b, -b + 0.05 * rng.standard_normal((n, 1))])
+    s = csr_fixed_nnz(rng, 40_000, 10, 5)
+    xs = np.abs(rng.standard_normal((10, 1))) * np.where(np.arange(10) % 3 == 0, -1.0, 1.0)[:, None]
+    bs = csr_matvec_fixed_order(s, xs, 5) + 0.05 * rng.standard_normal((40_000, 1))
+    return {"dense": (a, b, 0.5, 7), "dense_2col": (a, b2, 0.5, 8), "csr": (s, bs, 0.5, 9)}
+
+
+def lowrank_default_case():
+    """A 3000 x 2500 CSR at 2% density sampled from a rank-5 product plus
+    0.01 N(0,1) (config 5's construction, small): k = 5, eps = 0.5, seed = 11."""
+    rng = np.random.default_rng(53)
+    n, m, r = 3000, 2500, 5
+    u = rng.standard_normal((n, r))
+    v = rng.standard_normal((m, r))
+    pat = sp.random_array((n, m), density=0.02, rng=rng, format="coo")
+    vals = u[pat.row, 0] * v[pat.col, 0]
+    for j in range(1, r):
+        vals = vals + u[pat.row, j] * v[pat.col, j]
+    vals = vals + 0.01 * rng.standard_normal(vals.size)
+    return sp.csr_array((vals, (pat.row, pat.col)), shape=(n, m))

@@ -83,3 +83,75 @@ def test_gram_residual_matches_reference(name):
         c32, f32 = gram_residual_sq(a32, l, d, w)
         d32 = a32.toarray().astype(np.float64)
         assert abs(c32 - np.einsum("ij,ij->", d32 @ (w * d), l)) <= 1e-12 * f32
+
+
+NNLS = __import__("tests.synth", fromlist=["nnls_cases"]).nnls_cases()
+
+
+@pytest.mark.parametrize("name", sorted(NNLS))
+def test_nonneg_regression_matches_reference(name):
+    """SRHT o sparse embedding on the GPU (bit-identical sketches), the same
+    Lawson-Hanson steps on the host: x equal to the reference's up to LAPACK
+    rounding, the same active set, residual by the fused GPU pass."""
+    from paper_1207_6365_b200 import nonneg_regression
+
+    a, b, eps, seed = NNLS[name]
+    sol = nonneg_regression(a, b, eps, seed=seed)
+    ref_x = G[f"nnls_{name}/x"]
+    assert sol.method == "nnls" and sol.sketch_dim == int(G[f"nnls_{name}/sketch_dim"])
+    assert np.array_equal(sol.x > 0, ref_x > 0)
+    assert np.linalg.norm(sol.x - ref_x) <= 1e-10 * np.linalg.norm(ref_x)
+    ref_res = float(G[f"nnls_{name}/residual"])
+    assert abs(sol.residual_norm - ref_res) <= 1e-11 * ref_res
+
+
+def test_nnls_pass_cap_and_feasibility():
+    from paper_1207_6365_b200 import SolverError, lawson_hanson_nnls
+
+    rng = np.random.default_rng(0)
+    m = rng.standard_normal((50, 6))
+    y = rng.standard_normal(50)
+    x = lawson_hanson_nnls(m, y)
+    w = m.T @ (y - m @ x)
+    assert np.all(x >= 0) and np.all(w[x == 0] <= 1e-8 * max(np.abs(m.T @ y).max(), 1.0))
+    with pytest.raises(SolverError):
+        lawson_hanson_nnls(m, y @ np.zeros(50) + m @ np.ones(6), max_passes=0)
+
+
+def test_low_rank_default_strategy_matches_reference():
+    """low_rank_approx(a, k, eps) with the default srht_compose strategy:
+    column sketch (transpose-free) + SRHT, S U / S A + SRHT, all on the GPU and
+    bit-identical, so the factors equal the reference's; err from the fused
+    Gram pass (7.5M entries > the dense limit) to 1e-10."""
+    from paper_1207_6365_b200.lowrank import low_rank_approx
+
+    from .synth import lowrank_default_case
+
+    res = low_rank_approx(lowrank_default_case(), 5, 0.5, seed=11)
+    for key in ("l", "d", "w"):
+        assert np.array_equal(getattr(res.factors, key), G[f"lowrank_default/{key}"]), key
+    assert res.t_r == int(G["lowrank_default/t_r"]) and res.t_s == int(G["lowrank_default/t_s"])
+    assert res.cond_su == float(G["lowrank_default/cond_su"])
+    assert abs(res.err - float(G["lowrank_default/err"])) <= 1e-10 * float(G["lowrank_default/err"])
+    with pytest.raises(ValueError):
+        low_rank_approx(lowrank_default_case(), 5, 0.5, strategy="bogus")
+
+
+def test_srht_operator_views_and_apply():
+    from paper_1207_6365_b200 import SrhtOperator, srht_or_identity
+
+    z = np.load(os.path.join(GOLDEN, "srht_cases.npz"))
+    meta = z["meta"]
+    for k, (_, _, t, seed) in enumerate(meta):
+        a = z[f"a{k}"]
+        op = SrhtOperator(a.shape[0], int(t), int(seed))
+        assert np.array_equal(op.apply(a), z[f"y{k}"])
+        assert op.sign.shape == (op.n_pad,) and set(np.unique(op.sign)) <= {-1.0, 1.0}
+        assert op.sampled_rows.shape == (int(t),) and op.sampled_rows.max() < op.n_pad
+    op = SrhtOperator(1000, 300, 2)  # host views: the reference's arrays
+    assert np.array_equal(op.sign, G["srht_views/sign"]) and np.array_equal(op.sampled_rows, G["srht_views/rows"])
+    full = SrhtOperator(100, 1, 3, all_rows=True)  # exact isometry hook
+    x = np.random.default_rng(1).standard_normal((100, 4))
+    assert full.output_dim == 128
+    assert np.allclose(np.linalg.norm(full.apply(x)), np.linalg.norm(x), rtol=1e-13)
+    assert srht_or_identity(50, 60, 1).family == "identity"
