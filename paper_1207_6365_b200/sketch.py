@@ -570,7 +570,7 @@ def apply_right(a, s):
     other operator families keep the reference formula (S @ A^T)^T."""
     if isinstance(s, SparseEmbedding):
         return s.apply_right(a)
-    if isinstance(s, ComposedSketch) and isinstance(s.inner, SparseEmbedding):
+    if getattr(s, "family", None) == "composed" and isinstance(getattr(s, "inner", None), SparseEmbedding):
         # (outer inner A^T)^T = apply_right(A inner^T, outer): the sparse
         # embedding's column sketch stays transpose-free on the GPU
         y = s.inner.apply_right(a)

@@ -71,6 +71,7 @@ def test_shim_rebinds_reference_module_globals():
         lp = importlib.import_module("sketchnla.lp")
         assert ref.GeneralizedSparseEmbedding is skb.GeneralizedSparseEmbedding
         assert lp.GeneralizedSparseEmbedding is skb.GeneralizedSparseEmbedding
+        assert ref.SrhtOperator is skb.SrhtOperator
         # the reference factories resolve the class at call time (sketch.py:400,426,465)
         if not torch.cuda.is_available():
             with pytest.raises(Exception):
@@ -78,3 +79,4 @@ def test_shim_rebinds_reference_module_globals():
     finally:
         skb.uninstall()
     assert ref.SparseEmbedding is orig
+    assert ref.SrhtOperator is not skb.SrhtOperator
