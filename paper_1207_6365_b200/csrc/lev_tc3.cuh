@@ -35,6 +35,10 @@ inline size_t lev_tc3_smem(int dk, int k) {  // A: 128 x dk words; B: 2k x 2dk f
   return (size_t)kTcRows * dk * 4 + (size_t)(2 * k) * (2 * dk) * 2;
 }
 
+#ifndef SKT_TC3_BLOCKCLEAR
+#define SKT_TC3_BLOCKCLEAR 1
+#endif
+
 template <typename IP, typename IX, typename TS>
 __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d, int dk,
                                                              const IP *__restrict__ aip,
@@ -291,10 +295,12 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
                    : "memory");
     }
     // ---- overlap: the next tile's nonzeros and descriptors go in flight now
+#if !SKT_TC3_BLOCKCLEAR
     int cur_c[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) cur_c[i] = pc[i];
     const uint32_t longz = longm;
+#endif
     if (tile + gridDim.x < ntiles) load_data(rs_n, len_n);
     rs_c = rs_n;
     len_c = len_n;
@@ -329,6 +335,16 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
     const int64_t my_row = row0 + myr;
     const double unscale = __longlong_as_double((long long)(1023 + 2 * (rexp[myr] + pe)) << 52);
     if (my_row < n) scores[my_row] = (TS)((sc0 + sc1) * unscale);
+#if SKT_TC3_BLOCKCLEAR
+    // ---- clear this warp's 32 rows of the A tile: in every 16-byte K column
+    // they are one contiguous 512-byte block (16 r + 2048 (c / 4)), one
+    // 16-byte store per lane -- fewer instructions than re-zeroing the
+    // scattered entries, and no registers held across the MMA wait
+    {
+      unsigned char *blk = (unsigned char *)aw + warp * 512 + lane * 16;
+      for (int kc = 0; kc < dk / 4; ++kc) *(uint4 *)(blk + kc * (kTcRows * 16)) = make_uint4(0, 0, 0, 0);
+    }
+#else
     // ---- re-zero what this tile wrote
 #pragma unroll
     for (int i = 0; i < E; ++i)
@@ -337,6 +353,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
       const int r = __ffs(mm) - 1;
       for (int c = lane; c < dk; c += 32) aw[tc_off(warp * 32 + r, c, kTcRows) >> 2] = 0u;
     }
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();  // TMEM drained, tile clean, rexp read before the next densify
     asm volatile("tcgen05.fence::after_thread_sync;");
