@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "dense_g4.cuh"
 #include "dense_tma.cuh"
 
 namespace skt {
@@ -253,6 +254,15 @@ skt_status dispatch_g(const int64_t *indptr, const uint32_t *rows, uint64_t t, c
   return launch<TIn, TOut, VEC, 32>(indptr, rows, t, a, d, lda, sa, ldsa, flag, stream);
 }
 
+// SKT_DENSE_G4=0 disables the TMA gather4 kernel (A/B measurement).
+inline bool g4_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_DENSE_G4");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // SKT_DENSE_TMA=0 selects the register-gather kernel (A/B measurement).
 inline bool tma_enabled() {
   static const bool on = [] {
@@ -265,7 +275,7 @@ inline bool tma_enabled() {
 template <typename TIn, typename TOut>
 skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a_,
                         int64_t d, int64_t lda, void *sa_, int64_t ldsa, int32_t *flag,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int64_t n_rows_hint) {
   const TIn *a = (const TIn *)a_;
   TOut *sa = (TOut *)sa_;
   const uintptr_t ap = (uintptr_t)a;
@@ -276,6 +286,24 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
   // rows stay on the register gather: a 1D bulk copy costs ~46 SM cycles of TMA
   // issue, which caps 512 B rows at ~3.8 TB/s (measured, profiles/).
   const int64_t row_bytes = d * (int64_t)sizeof(TIn), lda_bytes = lda * (int64_t)sizeof(TIn);
+  // TMA gather4 (four random rows per TMA instruction): rows of 128 B .. 1 KB
+  // (16-byte multiples, <= 256 elements), row stride a 16-byte multiple
+  if (g4_enabled() && sizeof(TIn) == 4 && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 128 &&
+      row_bytes <= 1024 && d <= 256 && n_rows_hint > 0 && n_rows_hint < (1LL << 31)) {
+    CUtensorMap map;
+    if (make_row_map(&map, a, sizeof(TIn) == 8, n_rows_hint, d, lda_bytes)) {
+      const size_t smem = dense_g4_smem((int)row_bytes);
+      const int64_t blocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
+      auto k = row_bytes == 512    ? dense_g4_kernel<TOut, 1, true>
+               : row_bytes == 1024 ? dense_g4_kernel<TOut, 2, true>
+               : row_bytes < 512   ? dense_g4_kernel<TOut, 1, false>
+                                   : dense_g4_kernel<TOut, 2, false>;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_dense");
+      SKT_LAUNCH(k, (unsigned)blocks, kG4Warps * 32, smem, stream, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
+                 ldsa, flag);
+      return check_launch("skt_apply_dense");
+    }
+  }
   if (tma_enabled() && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 1024 &&
       row_bytes <= 2048) {
     const int kchunks = (int)((row_bytes + 511) / 512);
@@ -316,9 +344,9 @@ extern "C" skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *row
   if (!sa || (n > 0 && (!a || !rows))) return fail(SKT_EINVAL, fn, "NULL buffer");
   if (a_dtype == SKT_F32)
     return sa_dtype == SKT_F64
-               ? dispatch_vec<float, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream)
-               : dispatch_vec<float, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream);
+               ? dispatch_vec<float, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n)
+               : dispatch_vec<float, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n);
   return sa_dtype == SKT_F64
-             ? dispatch_vec<double, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream)
-             : dispatch_vec<double, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream);
+             ? dispatch_vec<double, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n)
+             : dispatch_vec<double, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n);
 }

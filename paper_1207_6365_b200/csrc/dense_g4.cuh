@@ -1,0 +1,205 @@
+// dense_g4.cuh -- K3 on TMA gather4: SA = S.A for dense row-major A whose rows
+// are 16-byte multiples of 128 B .. 1 KB (BASELINE config 3: 512 B rows).
+//
+// One warp per bucket.  Lane 0 issues cp.async.bulk.tensor.2d ... tile::gather4:
+// four rows at arbitrary row coordinates of A (the next four plan rows of the
+// bucket) land in one shared-memory stage per instruction, completion counted
+// in bytes on the stage's mbarrier.  A kG4Stages-deep ring per warp keeps 16
+// rows (8 KB at 512 B) in flight without holding registers, and the TMA engine
+// is issued once per 2 KB -- a 1D bulk copy per row is TMA-issue bound at
+// ~46 SM cycles per copy (3.8 TB/s on 512 B rows), gather4 is not
+// (tools/gather4_bench.cu: 7.15 TB/s for config 3's random rows incl. the fp64
+// accumulate, the streaming-read ceiling).
+//
+// The plan words (row | sign << 31) are read 32 at a time, coalesced, one
+// chunk ahead; the quad's rows and signs are broadcast with shuffles.  The
+// lanes consume a landed stage row by row: lane l owns the 16-byte column
+// chunks l, l + 32 of a row and adds s_i * A[i, cols] into fp64 accumulators in
+// ascending row order from +0.0 -- the reference's csr_matvecs order, so the
+// fp64 result is bit-identical.  The non-finite scan of as_dense is fused.
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+#include "dense_tma.cuh"
+
+namespace skt {
+namespace {
+
+#ifndef SKT_G4_WARPS
+#define SKT_G4_WARPS 4
+#endif
+#ifndef SKT_G4_STAGES
+#define SKT_G4_STAGES 6
+#endif
+constexpr int kG4Warps = SKT_G4_WARPS;
+constexpr int kG4Stages = SKT_G4_STAGES;  // quads in flight per warp (<= 8: issues stay within the next word chunk)
+
+__device__ __forceinline__ void g4_load(void *dst, const CUtensorMap *map, uint64_t *bar, int r0, int r1, int r2,
+                                        int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
+// s_i * A[i, 4 cols] into fp64: the sign is an XOR of the fp32 sign bits
+// (exact), then convert and add -- acc + (double)(s x), the reference's value
+__device__ __forceinline__ void g4_add(const uint4 &u, uint32_t m, double (&acc)[4]) {
+  acc[0] += (double)__uint_as_float(u.x ^ m);
+  acc[1] += (double)__uint_as_float(u.y ^ m);
+  acc[2] += (double)__uint_as_float(u.z ^ m);
+  acc[3] += (double)__uint_as_float(u.w ^ m);
+}
+
+// fp32 rows; K = 16-byte chunks per lane per row (row_bytes <= K * 512).
+// Finiteness: a non-finite input makes its column's fp64 sum non-finite (inf
+// stays inf, inf - inf and NaN give NaN) and finite fp32 inputs cannot
+// overflow an fp64 sum of < 2^31 rows, so the scan of as_dense is one test of
+// the accumulators per bucket instead of one per element.
+template <typename TOut, int K, bool kFull>
+__global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_constant__ CUtensorMap map,
+                                                                 const int64_t *__restrict__ indptr,
+                                                                 const uint32_t *__restrict__ rows, uint64_t t,
+                                                                 int row_bytes, int d, TOut *__restrict__ sa,
+                                                                 int64_t ldsa, int32_t *__restrict__ flag) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kG4Warps][kG4Stages];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t bucket = (int64_t)blockIdx.x * kG4Warps + w;
+  if (bucket >= (int64_t)t) return;
+  const int stage_bytes = 4 * row_bytes;                // the four rows, packed
+  const int stage_stride = (stage_bytes + 127) & ~127;  // TMA tensor destinations are 128-byte aligned
+  unsigned char *ring = smem_raw + (size_t)w * kG4Stages * stage_stride;
+  const uint32_t ring_s = smem_u32(ring) + 16u * lane;  // this lane's 16-byte column chunk
+  if (lane == 0)
+    for (int s = 0; s < kG4Stages; ++s) mbar_init(&bars[w][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+
+  const int64_t beg = indptr[bucket], end = indptr[bucket + 1];
+  const int nrows = (int)(end - beg);
+  const int nq = (nrows + 3) >> 2;
+  // plan words: lane j <-> position 32 c + j of the bucket (chunk c)
+  auto words = [&](int c) -> uint32_t {
+    const int p = 32 * c + lane;
+    return p < nrows ? __ldg(rows + beg + p) : 0u;
+  };
+  // chunk c (being consumed), c + 1 (issues run up to 4 quads ahead) and
+  // c + 2 (in flight: 12 quads of consumption to arrive)
+  uint32_t wc = words(0), wn = words(1), wn2 = words(2);
+  uint32_t sgn = __ballot_sync(0xffffffffu, (wc >> 31) != 0);  // sign bits of chunk c's rows
+  // issue quad q (its chunk is c0 = the chunk of the quad being consumed, or the next one)
+  auto issue = [&](int q, int c0) {
+    const uint32_t src = (q >> 3) == c0 ? wc : wn;
+    const int l0 = (4 * q) & 31;
+    int r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t wd = __shfl_sync(0xffffffffu, src, l0 + j);
+      // the last quad's padding slots fetch its first row again (never added)
+      r[j] = 4 * q + j < nrows ? (int)(wd & 0x7fffffffu) : r[0];
+    }
+    if (lane == 0) {
+      const int s = q % kG4Stages;
+      mbar_arrive_tx(&bars[w][s], (uint32_t)stage_bytes);
+      g4_load(ring + s * stage_stride, &map, &bars[w][s], r[0], r[1], r[2], r[3]);
+    }
+  };
+  for (int q = 0; q < kG4Stages && q < nq; ++q) issue(q, 0);
+
+  double acc[K][4];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[k][e] = 0.0;
+  for (int q = 0; q < nq; ++q) {
+    const int c = q >> 3;
+    if (q > 0 && (q & 7) == 0) {  // consumption enters chunk c: shift the word window
+      wc = wn;
+      wn = wn2;
+      wn2 = words(c + 2);
+      sgn = __ballot_sync(0xffffffffu, (wc >> 31) != 0);
+    }
+    const int s = q % kG4Stages;
+    mbar_wait(&bars[w][s], (uint32_t)((q / kG4Stages) & 1));
+    const uint32_t st = ring_s + (uint32_t)(s * stage_stride);
+    const uint32_t qs = sgn >> ((4 * q) & 31);  // bit j = sign of row 4q + j
+    const int cnt = nrows - 4 * q < 4 ? nrows - 4 * q : 4;
+    if (cnt == 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t m = ((qs >> j) & 1u) << 31;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (kFull || k * 512 + 16 * lane < row_bytes) g4_add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const uint32_t m = ((qs >> j) & 1u) << 31;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (kFull || k * 512 + 16 * lane < row_bytes) g4_add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+      }
+    }
+    __syncwarp();  // every lane is done with stage s before it is refilled
+    if (q + kG4Stages < nq) issue(q + kG4Stages, c);
+  }
+  bool bad = false;
+  TOut *o = sa + bucket * ldsa;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int col = (k * 32 + lane) * 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      bad |= !isfinite(acc[k][e]);
+      if (col + e < d) o[col + e] = (TOut)acc[k][e];
+    }
+  }
+  if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+inline size_t dense_g4_smem(int row_bytes) {
+  return (size_t)kG4Warps * kG4Stages * (((size_t)4 * row_bytes + 127) & ~(size_t)127);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+// 2D map over A (n rows x d elements, row stride lda_bytes), box = one row;
+// gather4 fetches four such boxes at arbitrary row coordinates
+inline bool make_row_map(CUtensorMap *map, const void *a, bool f64, int64_t n, int64_t d, int64_t lda_bytes) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  const cuuint64_t gstride[1] = {(cuuint64_t)lda_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)d, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(a),
+            gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+}  // namespace skt

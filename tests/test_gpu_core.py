@@ -267,6 +267,42 @@ def test_apply_torch_sparse_csr(rng):
     assert np.array_equal(op.apply(ta).cpu().numpy(), O.np_apply_csr(h, s, t, a))
 
 
+@pytest.mark.parametrize("d", [32, 36, 64, 128, 200, 256])
+def test_apply_dense_tma_gather4(d, rng, monkeypatch):
+    """fp32 rows of 128 B .. 1 KB go through the TMA gather4 kernel
+    (dense_g4.cuh): bit-identical to the reference order and to the register
+    kernel (SKT_DENSE_G4=0 only switches kernels inside the library, so the
+    A/B runs in one process through a fresh call), bucket ranges, partial last
+    quads, empty buckets, a strided view, and the fused finiteness check."""
+    n, t = 5003, 97
+    a = (rng.standard_normal((n, d)) * np.exp(rng.standard_normal((n, 1)))).astype(np.float32)
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    ref = O.apply_dense(h, s, t, a)
+    assert np.array_equal(op.apply(a), ref)
+    dev = torch.from_numpy(a).cuda()
+    for b0, b1 in [(0, 13), (13, 60), (60, 97)]:
+        part = op._apply_dense_device(dev, torch.float64, buckets=(b0, b1))
+        assert np.array_equal(part[b0:b1].cpu().numpy(), ref[b0:b1])
+    wide = torch.zeros((n, d + 8), dtype=torch.float32, device="cuda")
+    wide[:, :d] = dev
+    assert np.array_equal(op.apply(wide[:, :d]).cpu().numpy(), ref)  # lda = d + 8 (16-byte multiple)
+    sparse_op = SparseEmbedding(50, 40, seed=1)  # most buckets hold 0-3 rows
+    a2 = a[:50]
+    h2, s2 = O.hash_signs(50, 40, 1)
+    assert np.array_equal(sparse_op.apply(a2), O.apply_dense(h2, s2, 40, a2))
+    for bad in (np.nan, np.inf, -np.inf):
+        b = a.copy()
+        b[4321, d // 2] = bad
+        with pytest.raises(ValueError):
+            op.apply(b)
+    b = a.copy()  # +inf and -inf in the same bucket and column: NaN, still caught
+    rows = np.flatnonzero(h == h[0])[:2]
+    b[rows[0], 3], b[rows[1], 3] = np.inf, -np.inf
+    with pytest.raises(ValueError):
+        op.apply(b)
+
+
 def test_nonfinite_and_shape_errors(rng):
     op = SparseEmbedding(10, 4, seed=0)
     a = rng.standard_normal((10, 3))
