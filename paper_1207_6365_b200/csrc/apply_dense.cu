@@ -288,19 +288,19 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
   const int64_t row_bytes = d * (int64_t)sizeof(TIn), lda_bytes = lda * (int64_t)sizeof(TIn);
   // TMA gather4 (four random rows per TMA instruction): rows of 128 B .. 1 KB
   // (16-byte multiples, <= 256 elements), row stride a 16-byte multiple
-  if (g4_enabled() && sizeof(TIn) == 4 && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 128 &&
+  if (g4_enabled() && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 128 &&
       row_bytes <= 1024 && d <= 256 && n_rows_hint > 0 && n_rows_hint < (1LL << 31)) {
     CUtensorMap map;
     if (make_row_map(&map, a, sizeof(TIn) == 8, n_rows_hint, d, lda_bytes)) {
       const size_t smem = dense_g4_smem((int)row_bytes);
       const int64_t blocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
-      auto k = row_bytes == 512    ? dense_g4_kernel<TOut, 1, true>
-               : row_bytes == 1024 ? dense_g4_kernel<TOut, 2, true>
-               : row_bytes < 512   ? dense_g4_kernel<TOut, 1, false>
-                                   : dense_g4_kernel<TOut, 2, false>;
+      auto k = row_bytes == 512    ? dense_g4_kernel<TIn, TOut, 1, true>
+               : row_bytes == 1024 ? dense_g4_kernel<TIn, TOut, 2, true>
+               : row_bytes < 512   ? dense_g4_kernel<TIn, TOut, 1, false>
+                                   : dense_g4_kernel<TIn, TOut, 2, false>;
       SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_dense");
       SKT_LAUNCH(k, (unsigned)blocks, kG4Warps * 32, smem, stream, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
-                 ldsa, flag);
+                 ldsa, flag, (const unsigned char *)a, lda_bytes);
       return check_launch("skt_apply_dense");
     }
   }

@@ -51,26 +51,61 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
-// s_i * A[i, 4 cols] into fp64: the sign is an XOR of the fp32 sign bits
-// (exact), then convert and add -- acc + (double)(s x), the reference's value
-__device__ __forceinline__ void g4_add(const uint4 &u, uint32_t m, double (&acc)[4]) {
-  acc[0] += (double)__uint_as_float(u.x ^ m);
-  acc[1] += (double)__uint_as_float(u.y ^ m);
-  acc[2] += (double)__uint_as_float(u.z ^ m);
-  acc[3] += (double)__uint_as_float(u.w ^ m);
+// s_i * A[i, cols of one 16-byte chunk] into fp64: the sign is an XOR of the
+// sign bits (exact), then (fp32) convert and add -- acc + (double)(s x), the
+// reference's value
+template <typename TIn>
+struct G4;
+template <>
+struct G4<float> {
+  static constexpr int E = 4;
+  __device__ static __forceinline__ void add(const uint4 &u, uint32_t m, double (&acc)[4]) {
+    acc[0] += (double)__uint_as_float(u.x ^ m);
+    acc[1] += (double)__uint_as_float(u.y ^ m);
+    acc[2] += (double)__uint_as_float(u.z ^ m);
+    acc[3] += (double)__uint_as_float(u.w ^ m);
+  }
+};
+template <>
+struct G4<double> {
+  static constexpr int E = 2;
+  __device__ static __forceinline__ void add(const uint4 &u, uint32_t m, double (&acc)[2]) {
+    acc[0] += __longlong_as_double((long long)(((uint64_t)(u.y ^ m) << 32) | u.x));
+    acc[1] += __longlong_as_double((long long)(((uint64_t)(u.w ^ m) << 32) | u.z));
+  }
+};
+
+// Finiteness of the bucket's rows (as_dense's scan, _validation.py:25-26).
+// A non-finite input makes its column's fp64 sum non-finite (inf stays inf,
+// inf - inf and NaN give NaN), so only a bucket whose sums are not all finite
+// can hold one.  fp32 inputs cannot overflow an fp64 sum of < 2^31 rows, so
+// for them the test of the sums is exact; fp64 sums of finite values can
+// overflow, so such a bucket's rows are re-scanned element by element (rare).
+template <typename TIn>
+__device__ bool g4_rescan(const unsigned char *a, int64_t lda_bytes, const int64_t beg, int nrows,
+                          const uint32_t *__restrict__ rows, int row_bytes, int lane) {
+  bool bad = false;
+  for (int p = 0; p < nrows; ++p) {
+    const unsigned char *r = a + (int64_t)(__ldg(rows + beg + p) & 0x7fffffffu) * lda_bytes;
+    for (int off = 4 * lane; off < row_bytes; off += 128) {
+      const uint32_t w = *reinterpret_cast<const uint32_t *>(r + off);
+      if (sizeof(TIn) == 4) bad |= (w & 0x7f800000u) == 0x7f800000u;
+      else if (off & 4) bad |= (w & 0x7ff00000u) == 0x7ff00000u;  // the high word of each double
+    }
+  }
+  return __any_sync(0xffffffffu, bad);
 }
 
-// fp32 rows; K = 16-byte chunks per lane per row (row_bytes <= K * 512).
-// Finiteness: a non-finite input makes its column's fp64 sum non-finite (inf
-// stays inf, inf - inf and NaN give NaN) and finite fp32 inputs cannot
-// overflow an fp64 sum of < 2^31 rows, so the scan of as_dense is one test of
-// the accumulators per bucket instead of one per element.
-template <typename TOut, int K, bool kFull>
+// K = 16-byte chunks per lane per row (row_bytes <= K * 512).
+template <typename TIn, typename TOut, int K, bool kFull>
 __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const int64_t *__restrict__ indptr,
                                                                  const uint32_t *__restrict__ rows, uint64_t t,
                                                                  int row_bytes, int d, TOut *__restrict__ sa,
-                                                                 int64_t ldsa, int32_t *__restrict__ flag) {
+                                                                 int64_t ldsa, int32_t *__restrict__ flag,
+                                                                 const unsigned char *__restrict__ a_raw,
+                                                                 int64_t lda_bytes) {
+  constexpr int E = G4<TIn>::E;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[kG4Warps][kG4Stages];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -116,11 +151,11 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   };
   for (int q = 0; q < kG4Stages && q < nq; ++q) issue(q, 0);
 
-  double acc[K][4];
+  double acc[K][E];
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[k][e] = 0.0;
+    for (int e = 0; e < E; ++e) acc[k][e] = 0.0;
   for (int q = 0; q < nq; ++q) {
     const int c = q >> 3;
     if (q > 0 && (q & 7) == 0) {  // consumption enters chunk c: shift the word window
@@ -140,14 +175,14 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
         const uint32_t m = ((qs >> j) & 1u) << 31;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          if (kFull || k * 512 + 16 * lane < row_bytes) g4_add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+          if (kFull || k * 512 + 16 * lane < row_bytes) G4<TIn>::add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
       }
     } else {
       for (int j = 0; j < cnt; ++j) {
         const uint32_t m = ((qs >> j) & 1u) << 31;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          if (kFull || k * 512 + 16 * lane < row_bytes) g4_add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+          if (kFull || k * 512 + 16 * lane < row_bytes) G4<TIn>::add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
       }
     }
     __syncwarp();  // every lane is done with stage s before it is refilled
@@ -157,14 +192,17 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   TOut *o = sa + bucket * ldsa;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const int col = (k * 32 + lane) * 4;
+    const int col = (k * 32 + lane) * E;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < E; ++e) {
       bad |= !isfinite(acc[k][e]);
       if (col + e < d) o[col + e] = (TOut)acc[k][e];
     }
   }
-  if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+  if (flag && __any_sync(0xffffffffu, bad)) {
+    const bool real = sizeof(TIn) == 4 || g4_rescan<TIn>(a_raw, lda_bytes, beg, nrows, rows, row_bytes, lane);
+    if (real && lane == 0) atomicOr(flag, 1);
+  }
 }
 
 inline size_t dense_g4_smem(int row_bytes) {

@@ -267,15 +267,17 @@ def test_apply_torch_sparse_csr(rng):
     assert np.array_equal(op.apply(ta).cpu().numpy(), O.np_apply_csr(h, s, t, a))
 
 
-@pytest.mark.parametrize("d", [32, 36, 64, 128, 200, 256])
-def test_apply_dense_tma_gather4(d, rng, monkeypatch):
+@pytest.mark.parametrize("dtype,d", [(np.float32, 32), (np.float32, 36), (np.float32, 64), (np.float32, 128),
+                                     (np.float32, 200), (np.float32, 256), (np.float64, 16), (np.float64, 20),
+                                     (np.float64, 64), (np.float64, 100), (np.float64, 128)])
+def test_apply_dense_tma_gather4(dtype, d, rng, monkeypatch):
     """fp32 rows of 128 B .. 1 KB go through the TMA gather4 kernel
     (dense_g4.cuh): bit-identical to the reference order and to the register
     kernel (SKT_DENSE_G4=0 only switches kernels inside the library, so the
     A/B runs in one process through a fresh call), bucket ranges, partial last
     quads, empty buckets, a strided view, and the fused finiteness check."""
     n, t = 5003, 97
-    a = (rng.standard_normal((n, d)) * np.exp(rng.standard_normal((n, 1)))).astype(np.float32)
+    a = (rng.standard_normal((n, d)) * np.exp(rng.standard_normal((n, 1)))).astype(dtype)
     op = SparseEmbedding(n, t, seed=d)
     h, s = O.hash_signs(n, t, d)
     ref = O.apply_dense(h, s, t, a)
@@ -284,7 +286,7 @@ def test_apply_dense_tma_gather4(d, rng, monkeypatch):
     for b0, b1 in [(0, 13), (13, 60), (60, 97)]:
         part = op._apply_dense_device(dev, torch.float64, buckets=(b0, b1))
         assert np.array_equal(part[b0:b1].cpu().numpy(), ref[b0:b1])
-    wide = torch.zeros((n, d + 8), dtype=torch.float32, device="cuda")
+    wide = torch.zeros((n, d + 8), dtype=dev.dtype, device="cuda")
     wide[:, :d] = dev
     assert np.array_equal(op.apply(wide[:, :d]).cpu().numpy(), ref)  # lda = d + 8 (16-byte multiple)
     sparse_op = SparseEmbedding(50, 40, seed=1)  # most buckets hold 0-3 rows
@@ -301,6 +303,12 @@ def test_apply_dense_tma_gather4(d, rng, monkeypatch):
     b[rows[0], 3], b[rows[1], 3] = np.inf, -np.inf
     with pytest.raises(ValueError):
         op.apply(b)
+    if dtype == np.float64:  # finite values whose fp64 sum overflows: no error, inf in SA (as the reference)
+        b = a.copy()
+        same = np.flatnonzero((h == h[0]) & (s == s[np.flatnonzero(h == h[0])[0]]))[:2]  # same bucket, same sign
+        b[same, 5] = 1.5e308
+        got = op.apply(b)
+        assert np.isinf(got[h[0], 5]) and np.array_equal(got, O.apply_dense(h, s, t, b))
 
 
 def test_nonfinite_and_shape_errors(rng):
