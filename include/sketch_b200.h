@@ -243,13 +243,14 @@ skt_status skt_srht_apply(const double *a, int64_t n, int64_t d, int64_t lda, co
  * sorts the virtual rows, skt_gse_fold_rows rewrites plan words to j.
  * skt_gse_apply_dense / _csr compute SA = self._mat @ a (sketch.py:222-227)
  * with scipy's per-element order and rounding (fp64, products rounded, no FMA:
- * bit-identical); SA is fp64 t x d (ldsa). */
+ * bit-identical); SA is fp64 t x d (ldsa).  Dense A has n rows (rows of
+ * 128 B .. 1 KB use K3's TMA gather4 kernel with weighted terms, |weight| <= 1). */
 skt_status skt_gse_buckets(const uint32_t *outer, const uint32_t *inner, int64_t n, int32_t k, uint32_t v,
                            uint64_t q, uint32_t *h, void *stream);
 skt_status skt_gse_fold_rows(uint32_t *rows, int64_t count, int64_t n, void *stream);
-skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a,
-                               skt_dtype a_dtype, int64_t d, int64_t lda, double weight, double *sa,
-                               int64_t ldsa, int32_t *nonfinite_flag, void *stream);
+skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                               const void *a, skt_dtype a_dtype, int64_t d, int64_t lda, double weight,
+                               double *sa, int64_t ldsa, int32_t *nonfinite_flag, void *stream);
 skt_status skt_gse_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a_indptr,
                              skt_itype indptr_type, const void *a_indices, skt_itype index_type,
                              const void *a_vals, skt_dtype val_dtype, int64_t d, double weight, double *sa,

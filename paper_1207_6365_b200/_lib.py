@@ -150,7 +150,7 @@ def lib() -> ctypes.CDLL:
         "skt_srht_apply": ([P, i64, i64, i64, P, P, i64, ctypes.c_double, P, i64, P, sz, P], i32),
         "skt_gse_buckets": ([P, P, i64, i32, u32, u64, P, P], i32),
         "skt_gse_fold_rows": ([P, i64, i64, P], i32),
-        "skt_gse_apply_dense": ([P, P, u64, P, i32, i64, i64, ctypes.c_double, P, i64, P, P], i32),
+        "skt_gse_apply_dense": ([P, P, u64, i64, P, i32, i64, i64, ctypes.c_double, P, i64, P, P], i32),
         "skt_gse_apply_csr": ([P, P, u64, P, i32, P, i32, P, i32, i64, ctypes.c_double, P, i64, P], i32),
         "skt_mm_probe": ([ctypes.c_char_p, ctypes.POINTER(SktMmInfo)], i32),
         "skt_mm_read_coo": ([ctypes.c_char_p, i64, P, P, P, ctypes.POINTER(i64), i32], i32),

@@ -286,26 +286,32 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
   // rows stay on the register gather: a 1D bulk copy costs ~46 SM cycles of TMA
   // issue, which caps 512 B rows at ~3.8 TB/s (measured, profiles/).
   const int64_t row_bytes = d * (int64_t)sizeof(TIn), lda_bytes = lda * (int64_t)sizeof(TIn);
-  // TMA gather4 (four random rows per TMA instruction): rows of 128 B .. 1 KB
-  // (16-byte multiples, <= 256 elements), row stride a 16-byte multiple
-  if (g4_enabled() && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 128 &&
-      row_bytes <= 1024 && d <= 256 && n_rows_hint > 0 && n_rows_hint < (1LL << 31)) {
+  // TMA gather4 (four random rows per TMA instruction): rows of 512 B .. 2 KB
+  // (16-byte multiples; one box of <= 256 elements or two equal boxes), row
+  // stride a 16-byte multiple.  Measured (tools/dense_rowsize.py, 8.6 GB
+  // inputs): 512 B rows 1.24 ms vs 1.41 ms for the register gather, 1 KB 1.24
+  // vs 5.5 ms (1D bulk copies); 256 B rows break even and 128 B rows are
+  // faster on the register gather.
+  const int nbox = g4_boxes(d, (int64_t)sizeof(TIn));
+  if (g4_enabled() && nbox > 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && n_rows_hint > 0 &&
+      n_rows_hint < (1LL << 31)) {
     CUtensorMap map;
-    if (make_row_map(&map, a, sizeof(TIn) == 8, n_rows_hint, d, lda_bytes)) {
+    if (make_row_map(&map, a, sizeof(TIn) == 8, n_rows_hint, d, lda_bytes, d / nbox)) {
       const size_t smem = dense_g4_smem((int)row_bytes);
       const int64_t blocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
       auto k = row_bytes == 512    ? dense_g4_kernel<TIn, TOut, 1, true>
                : row_bytes == 1024 ? dense_g4_kernel<TIn, TOut, 2, true>
-               : row_bytes < 512   ? dense_g4_kernel<TIn, TOut, 1, false>
-                                   : dense_g4_kernel<TIn, TOut, 2, false>;
+               : row_bytes == 2048 ? dense_g4_kernel<TIn, TOut, 4, true>
+               : row_bytes < 1024  ? dense_g4_kernel<TIn, TOut, 2, false>
+                                   : dense_g4_kernel<TIn, TOut, 4, false>;
       SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_dense");
       SKT_LAUNCH(k, (unsigned)blocks, kG4Warps * 32, smem, stream, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
-                 ldsa, flag, (const unsigned char *)a, lda_bytes);
+                 ldsa, flag, (const unsigned char *)a, lda_bytes, 0.0, nbox);
       return check_launch("skt_apply_dense");
     }
   }
   if (tma_enabled() && row_bytes % 16 == 0 && lda_bytes % 16 == 0 && ap % 16 == 0 && row_bytes >= 1024 &&
-      row_bytes <= 2048) {
+      row_bytes <= 2048 && dense_tma_smem((int)row_bytes) <= 200 * 1024) {  // (its ring outgrows smem above 1.6 KB)
     const int kchunks = (int)((row_bytes + 511) / 512);
     const size_t smem = dense_tma_smem((int)row_bytes);
     const int64_t blocks = ((int64_t)t + kTmaWarps - 1) / kTmaWarps;

@@ -36,12 +36,12 @@ namespace {
 constexpr int kG4Warps = SKT_G4_WARPS;
 constexpr int kG4Stages = SKT_G4_STAGES;  // quads in flight per warp (<= 8: issues stay within the next word chunk)
 
-__device__ __forceinline__ void g4_load(void *dst, const CUtensorMap *map, uint64_t *bar, int r0, int r1, int r2,
-                                        int r3) {
+__device__ __forceinline__ void g4_load(void *dst, const CUtensorMap *map, uint64_t *bar, int col, int r0, int r1,
+                                        int r2, int r3) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -65,6 +65,13 @@ struct G4<float> {
     acc[2] += (double)__uint_as_float(u.z ^ m);
     acc[3] += (double)__uint_as_float(u.w ^ m);
   }
+  // weighted (generalized embedding): acc + fl(w (s x)), no fused multiply-add
+  __device__ static __forceinline__ void add_w(const uint4 &u, uint32_t m, double w, double (&acc)[4]) {
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(w, (double)__uint_as_float(u.x ^ m)));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(w, (double)__uint_as_float(u.y ^ m)));
+    acc[2] = __dadd_rn(acc[2], __dmul_rn(w, (double)__uint_as_float(u.z ^ m)));
+    acc[3] = __dadd_rn(acc[3], __dmul_rn(w, (double)__uint_as_float(u.w ^ m)));
+  }
 };
 template <>
 struct G4<double> {
@@ -73,12 +80,24 @@ struct G4<double> {
     acc[0] += __longlong_as_double((long long)(((uint64_t)(u.y ^ m) << 32) | u.x));
     acc[1] += __longlong_as_double((long long)(((uint64_t)(u.w ^ m) << 32) | u.z));
   }
+  __device__ static __forceinline__ void add_w(const uint4 &u, uint32_t m, double w, double (&acc)[2]) {
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(w, __longlong_as_double((long long)(((uint64_t)(u.y ^ m) << 32) | u.x))));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(w, __longlong_as_double((long long)(((uint64_t)(u.w ^ m) << 32) | u.z))));
+  }
 };
+
+template <typename TIn, bool kW>
+__device__ __forceinline__ void g4_term(const uint4 &u, uint32_t m, double w, double (&acc)[G4<TIn>::E]) {
+  if (kW)
+    G4<TIn>::add_w(u, m, w, acc);
+  else
+    G4<TIn>::add(u, m, acc);
+}
 
 // Finiteness of the bucket's rows (as_dense's scan, _validation.py:25-26).
 // A non-finite input makes its column's fp64 sum non-finite (inf stays inf,
-// inf - inf and NaN give NaN), so only a bucket whose sums are not all finite
-// can hold one.  fp32 inputs cannot overflow an fp64 sum of < 2^31 rows, so
+// inf - inf and NaN give NaN; a weight |w| <= 1 keeps finite terms finite), so
+// only a bucket whose sums are not all finite can hold one.  fp32 inputs cannot overflow an fp64 sum of < 2^31 rows, so
 // for them the test of the sums is exact; fp64 sums of finite values can
 // overflow, so such a bucket's rows are re-scanned element by element (rare).
 template <typename TIn>
@@ -96,15 +115,19 @@ __device__ bool g4_rescan(const unsigned char *a, int64_t lda_bytes, const int64
   return __any_sync(0xffffffffu, bad);
 }
 
-// K = 16-byte chunks per lane per row (row_bytes <= K * 512).
-template <typename TIn, typename TOut, int K, bool kFull>
+// K = 16-byte chunks per lane per row (row_bytes <= K * 512).  A row is fetched
+// as nbox (1 or 2) column boxes of row_bytes / nbox (a box is <= 256 elements,
+// 1 KB); a stage holds box b's four rows at b * 4 * box_bytes.
+// kW: every term weighted by w (the generalized embedding's 1/sqrt(k), with
+// the reference's separate rounding of the product), otherwise w is unused.
+template <typename TIn, typename TOut, int K, bool kFull, bool kW = false>
 __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const int64_t *__restrict__ indptr,
                                                                  const uint32_t *__restrict__ rows, uint64_t t,
                                                                  int row_bytes, int d, TOut *__restrict__ sa,
                                                                  int64_t ldsa, int32_t *__restrict__ flag,
                                                                  const unsigned char *__restrict__ a_raw,
-                                                                 int64_t lda_bytes) {
+                                                                 int64_t lda_bytes, double wgt, int nbox) {
   constexpr int E = G4<TIn>::E;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[kG4Warps][kG4Stages];
@@ -114,7 +137,18 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   const int stage_bytes = 4 * row_bytes;                // the four rows, packed
   const int stage_stride = (stage_bytes + 127) & ~127;  // TMA tensor destinations are 128-byte aligned
   unsigned char *ring = smem_raw + (size_t)w * kG4Stages * stage_stride;
-  const uint32_t ring_s = smem_u32(ring) + 16u * lane;  // this lane's 16-byte column chunk
+  const uint32_t ring_s = smem_u32(ring);
+  const int box_bytes = row_bytes / nbox, box_elems = d / nbox;
+  // this lane's 16-byte column chunks: offset inside a stage (row 0) per k
+  uint32_t loff[K];
+  bool lval[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int o = k * 512 + 16 * lane;
+    lval[k] = kFull || o < row_bytes;
+    const int b = o >= box_bytes ? 1 : 0;
+    loff[k] = (uint32_t)(b * 4 * box_bytes + (o - b * box_bytes));
+  }
   if (lane == 0)
     for (int s = 0; s < kG4Stages; ++s) mbar_init(&bars[w][s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -146,7 +180,8 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
     if (lane == 0) {
       const int s = q % kG4Stages;
       mbar_arrive_tx(&bars[w][s], (uint32_t)stage_bytes);
-      g4_load(ring + s * stage_stride, &map, &bars[w][s], r[0], r[1], r[2], r[3]);
+      for (int b = 0; b < nbox; ++b)
+        g4_load(ring + s * stage_stride + b * 4 * box_bytes, &map, &bars[w][s], b * box_elems, r[0], r[1], r[2], r[3]);
     }
   };
   for (int q = 0; q < kG4Stages && q < nq; ++q) issue(q, 0);
@@ -175,14 +210,14 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
         const uint32_t m = ((qs >> j) & 1u) << 31;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          if (kFull || k * 512 + 16 * lane < row_bytes) G4<TIn>::add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+          if (lval[k]) g4_term<TIn, kW>(lds128(st + loff[k] + j * box_bytes), m, wgt, acc[k]);
       }
     } else {
       for (int j = 0; j < cnt; ++j) {
         const uint32_t m = ((qs >> j) & 1u) << 31;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          if (kFull || k * 512 + 16 * lane < row_bytes) G4<TIn>::add(lds128(st + j * row_bytes + k * 512), m, acc[k]);
+          if (lval[k]) g4_term<TIn, kW>(lds128(st + loff[k] + j * box_bytes), m, wgt, acc[k]);
       }
     }
     __syncwarp();  // every lane is done with stage s before it is refilled
@@ -205,6 +240,15 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   }
 }
 
+// rows the gather4 kernels take: 512 B .. 2 KB, 16-byte multiples, as one box
+// (<= 1 KB) or two equal boxes (each a 16-byte multiple); returns nbox or 0
+inline int g4_boxes(int64_t d, int64_t esz) {
+  const int64_t rb = d * esz;
+  if (rb < 512 || rb > 2048 || rb % 16) return 0;
+  if (rb <= 1024) return 1;
+  return (d % 2 == 0 && (rb / 2) % 16 == 0) ? 2 : 0;
+}
+
 inline size_t dense_g4_smem(int row_bytes) {
   return (size_t)kG4Warps * kG4Stages * (((size_t)4 * row_bytes + 127) & ~(size_t)127);
 }
@@ -225,14 +269,15 @@ inline EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 2D map over A (n rows x d elements, row stride lda_bytes), box = one row;
-// gather4 fetches four such boxes at arbitrary row coordinates
-inline bool make_row_map(CUtensorMap *map, const void *a, bool f64, int64_t n, int64_t d, int64_t lda_bytes) {
+// 2D map over A (n rows x d elements, row stride lda_bytes), box = one row's
+// box_elems columns; gather4 fetches four such boxes at arbitrary row coordinates
+inline bool make_row_map(CUtensorMap *map, const void *a, bool f64, int64_t n, int64_t d, int64_t lda_bytes,
+                         int64_t box_elems) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
   const cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)n};
   const cuuint64_t gstride[1] = {(cuuint64_t)lda_bytes};
-  const cuuint32_t box[2] = {(cuuint32_t)d, 1};
+  const cuuint32_t box[2] = {(cuuint32_t)box_elems, 1};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(a),
             gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

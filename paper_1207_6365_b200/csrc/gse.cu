@@ -19,7 +19,10 @@
 // exactly that (__dmul_rn + __dadd_rn), so the result is bit-identical.
 #include <type_traits>
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "dense_g4.cuh"
 
 namespace skt {
 namespace {
@@ -167,16 +170,43 @@ extern "C" skt_status skt_gse_fold_rows(uint32_t *rows, int64_t count, int64_t n
   return check_launch(fn);
 }
 
-extern "C" skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t, const void *a,
-                                          skt_dtype a_dtype, int64_t d, int64_t lda, double weight, double *sa,
-                                          int64_t ldsa, int32_t *nonfinite_flag, void *stream_) {
+extern "C" skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                                          const void *a, skt_dtype a_dtype, int64_t d, int64_t lda, double weight,
+                                          double *sa, int64_t ldsa, int32_t *nonfinite_flag, void *stream_) {
   static const char *fn = "skt_gse_apply_dense";
-  if (!indptr || t < 1 || d < 0 || lda < d || ldsa < d || (a_dtype != SKT_F32 && a_dtype != SKT_F64))
+  if (!indptr || t < 1 || n < 0 || d < 0 || lda < d || ldsa < d || (a_dtype != SKT_F32 && a_dtype != SKT_F64) ||
+      !(fabs(weight) <= 1.0))
     return fail(SKT_EINVAL, fn, "bad arguments");
   cudaStream_t st = as_stream(stream_);
   if (nonfinite_flag) SKT_CUDA_TRY(cudaMemsetAsync(nonfinite_flag, 0, sizeof(int32_t), st), fn);
   if (d == 0) return SKT_OK;
   if (!sa) return fail(SKT_EINVAL, fn, "NULL output");
+  // rows of 512 B .. 2 KB: the K3 TMA gather4 kernel with weighted terms
+  {
+    const int64_t esz = a_dtype == SKT_F32 ? 4 : 8, row_bytes = d * esz, lda_bytes = lda * esz;
+    const int nbox = g4_boxes(d, esz);
+    const char *g4e = getenv("SKT_DENSE_G4");
+    CUtensorMap map;
+    if (!(g4e && g4e[0] == '0') && nbox > 0 && lda_bytes % 16 == 0 && (uintptr_t)a % 16 == 0 && n > 0 &&
+        n < (1LL << 31) && make_row_map(&map, a, a_dtype == SKT_F64, n, d, lda_bytes, d / nbox)) {
+      const size_t smem = dense_g4_smem((int)row_bytes);
+      const int64_t gblocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
+      typedef void (*KFn)(const CUtensorMap, const int64_t *, const uint32_t *, uint64_t, int, int, double *, int64_t,
+                          int32_t *, const unsigned char *, int64_t, double, int);
+#define SKT_G4W(TIN)                                                                \
+  (row_bytes == 512    ? (KFn)dense_g4_kernel<TIN, double, 1, true, true>           \
+   : row_bytes == 1024 ? (KFn)dense_g4_kernel<TIN, double, 2, true, true>           \
+   : row_bytes == 2048 ? (KFn)dense_g4_kernel<TIN, double, 4, true, true>           \
+   : row_bytes < 1024  ? (KFn)dense_g4_kernel<TIN, double, 2, false, true>          \
+                       : (KFn)dense_g4_kernel<TIN, double, 4, false, true>)
+      const KFn k = a_dtype == SKT_F32 ? SKT_G4W(float) : SKT_G4W(double);
+#undef SKT_G4W
+      SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+      SKT_LAUNCH(k, (unsigned)gblocks, kG4Warps * 32, smem, st, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
+                 ldsa, nonfinite_flag, (const unsigned char *)a, lda_bytes, weight, nbox);
+      return check_launch(fn);
+    }
+  }
   const int64_t blocks = ((int64_t)t + kGseWarps - 1) / kGseWarps;
   if (a_dtype == SKT_F32)
     SKT_LAUNCH(gse_dense_kernel<float>, (unsigned)blocks, kGseWarps * 32, 0, st, indptr, rows, t, (const float *)a,

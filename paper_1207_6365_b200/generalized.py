@@ -166,7 +166,8 @@ class GeneralizedSparseEmbedding(SketchOperator):
                 x = x.reshape(x.shape[0], -1).contiguous()
                 d = x.shape[1]
                 out = torch.empty((self.output_dim, d), dtype=torch.float64, device=dev)
-                check(L.skt_gse_apply_dense(_ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim, _ptr(x),
+                check(L.skt_gse_apply_dense(_ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim,
+                                            x.shape[0], _ptr(x),
                                             _TORCH_TO_SKT[x.dtype], d, max(d, 1), self.scale, _ptr(out), max(d, 1),
                                             None, stream))
                 if one_d:

@@ -267,12 +267,13 @@ def test_apply_torch_sparse_csr(rng):
     assert np.array_equal(op.apply(ta).cpu().numpy(), O.np_apply_csr(h, s, t, a))
 
 
-@pytest.mark.parametrize("dtype,d", [(np.float32, 32), (np.float32, 36), (np.float32, 64), (np.float32, 128),
-                                     (np.float32, 200), (np.float32, 256), (np.float64, 16), (np.float64, 20),
-                                     (np.float64, 64), (np.float64, 100), (np.float64, 128)])
+@pytest.mark.parametrize("dtype,d", [(np.float32, 32), (np.float32, 64), (np.float32, 128), (np.float32, 144),
+                                     (np.float32, 200), (np.float32, 256), (np.float32, 272), (np.float32, 384),
+                                     (np.float32, 512), (np.float64, 20), (np.float64, 64), (np.float64, 100),
+                                     (np.float64, 128), (np.float64, 192), (np.float64, 256)])
 def test_apply_dense_tma_gather4(dtype, d, rng, monkeypatch):
-    """fp32 rows of 128 B .. 1 KB go through the TMA gather4 kernel
-    (dense_g4.cuh): bit-identical to the reference order and to the register
+    """Rows of 512 B .. 2 KB go through the TMA gather4 kernel (dense_g4.cuh;
+    one or two column boxes per row), smaller ones through the register gather: bit-identical to the reference order and to the register
     kernel (SKT_DENSE_G4=0 only switches kernels inside the library, so the
     A/B runs in one process through a fresh call), bucket ranges, partial last
     quads, empty buckets, a strided view, and the fused finiteness check."""
@@ -309,6 +310,18 @@ def test_apply_dense_tma_gather4(dtype, d, rng, monkeypatch):
         b[same, 5] = 1.5e308
         got = op.apply(b)
         assert np.isinf(got[h[0], 5]) and np.array_equal(got, O.apply_dense(h, s, t, b))
+
+
+@pytest.mark.parametrize("d", [452, 500])
+def test_apply_dense_rows_beyond_gather4(d, rng, monkeypatch):
+    """fp32 rows of 1.8-2 KB that gather4 does not take (d not a multiple of 8)
+    fall back to a kernel that fits shared memory; with gather4 disabled the
+    2 KB rows too."""
+    n, t = 2000, 37
+    a = rng.standard_normal((n, d)).astype(np.float32)
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    assert np.array_equal(op.apply(a), O.apply_dense(h, s, t, a))
 
 
 def test_nonfinite_and_shape_errors(rng):

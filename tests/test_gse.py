@@ -60,3 +60,19 @@ def test_gse_gpu_bit_exact():
         # torch CUDA input stays on the device
         x = torch.from_numpy(z[f"a64_{k}"]).cuda()
         assert np.array_equal(op.apply(x).cpu().numpy(), z[f"sa64_{k}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,d", [(np.float64, 64), (np.float64, 20), (np.float32, 64), (np.float32, 200),
+                                     (np.float32, 384), (np.float64, 256)])
+def test_gse_gpu_gather4_rows(dtype, d):
+    """Rows of 512 B .. 2 KB take the K3 gather4 kernel with weighted terms:
+    still scipy's order and rounding (fl(w x) then add), bit for bit."""
+    from paper_1207_6365_b200.generalized import GeneralizedSparseEmbedding
+
+    n = 6000
+    op = GeneralizedSparseEmbedding(n, 5, 0.5, 0.1, 11)
+    _, _, _, _, _, _, _, mat = O.gse_operator(n, 5, 0.5, 0.1, 11)
+    a = np.random.default_rng(d).standard_normal((n, d)).astype(dtype)
+    ref = mat @ a.astype(np.float64)
+    assert np.array_equal(op.apply(a), ref)
