@@ -137,17 +137,23 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   const int stage_bytes = 4 * row_bytes;                // the four rows, packed
   const int stage_stride = (stage_bytes + 127) & ~127;  // TMA tensor destinations are 128-byte aligned
   unsigned char *ring = smem_raw + (size_t)w * kG4Stages * stage_stride;
-  const uint32_t ring_s = smem_u32(ring);
-  const int box_bytes = row_bytes / nbox, box_elems = d / nbox;
-  // this lane's 16-byte column chunks: offset inside a stage (row 0) per k
+  // two column boxes only for rows > 1 KB (K = 4); otherwise one box = the row
+  const int box_bytes = K > 2 ? row_bytes / nbox : row_bytes, box_elems = K > 2 ? d / nbox : d;
+  // this lane's 16-byte column chunks: offset inside a stage (row 0) per k,
+  // the lane's own offset folded into the ring base when there is one box
+  const uint32_t ring_s = smem_u32(ring) + (K > 2 ? 0u : 16u * lane);
   uint32_t loff[K];
   bool lval[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int o = k * 512 + 16 * lane;
     lval[k] = kFull || o < row_bytes;
-    const int b = o >= box_bytes ? 1 : 0;
-    loff[k] = (uint32_t)(b * 4 * box_bytes + (o - b * box_bytes));
+    if (K > 2) {
+      const int b = o >= box_bytes ? 1 : 0;
+      loff[k] = (uint32_t)(b * 4 * box_bytes + (o - b * box_bytes));
+    } else {
+      loff[k] = (uint32_t)(k * 512);
+    }
   }
   if (lane == 0)
     for (int s = 0; s < kG4Stages; ++s) mbar_init(&bars[w][s], 1);
@@ -180,8 +186,9 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
     if (lane == 0) {
       const int s = q % kG4Stages;
       mbar_arrive_tx(&bars[w][s], (uint32_t)stage_bytes);
-      for (int b = 0; b < nbox; ++b)
-        g4_load(ring + s * stage_stride + b * 4 * box_bytes, &map, &bars[w][s], b * box_elems, r[0], r[1], r[2], r[3]);
+      g4_load(ring + s * stage_stride, &map, &bars[w][s], 0, r[0], r[1], r[2], r[3]);
+      if (K > 2 && nbox > 1)
+        g4_load(ring + s * stage_stride + 4 * box_bytes, &map, &bars[w][s], box_elems, r[0], r[1], r[2], r[3]);
     }
   };
   for (int q = 0; q < kG4Stages && q < nq; ++q) issue(q, 0);
