@@ -347,7 +347,7 @@ def our_arm(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or (args.fused and "RANK" in os.environ):
         dist.init_process_group("nccl", device_id=dev)
     n, d, m = cfg["n"], cfg["d"], cfg["m"]
     # config 5 at N > 1: bucket ownership -- every rank holds the
@@ -418,12 +418,22 @@ def our_arm(args, cfg):
     # N > 1, dense: pipelined exchange -- SA is computed in contiguous bucket
     # ranges and each range is all-reduced (async, NCCL stream) while the next
     # range is computed (distributed.ShardedSparseEmbedding.apply(chunks=K)).
-    pipelined = world > 1 and cfg["kind"] == "dense" and lev is None and args.chunks > 1
+    fused = None
+    if args.fused and cfg["kind"] == "dense" and lev is None and dist.is_initialized():
+        from paper_1207_6365_b200.distributed import FusedShardedSparseEmbedding
+
+        fused = FusedShardedSparseEmbedding(n, m, cfg["seed"], device=dev)
+    pipelined = world > 1 and cfg["kind"] == "dense" and lev is None and args.chunks > 1 and fused is None
     ranges = [(k * m // args.chunks, (k + 1) * m // args.chunks) for k in range(args.chunks)]
 
     def step(kev=None):
         if kev is not None:
             kev[0].record(stream)
+        if fused is not None:
+            fused.apply(A, sa_dt)
+            if kev is not None:
+                kev[1].record(stream)
+            return
         if pipelined:
             works = []
             for c0, c1 in ranges:
@@ -561,14 +571,17 @@ def our_arm(args, cfg):
                    "l2": ("L2 flushed before every step (512 MB write, outside the per-step events)" if flush_l2
                           else "inputs larger than L2 (no flush needed)"),
                    "parallelism": (f"bucket-ownership x{world}: rank owns SA rows [{b0}, {b1}), whole input on "
-                                   "every rank, no collective") if bucket_mode else f"row-shard x{world}" + (
+                                   "every rank, no collective") if bucket_mode else
+                                  (f"row-shard x{world} + exchange fused into K3 (push to owner slots over "
+                                   "symmetric memory, slot sums, all-gather)") if fused is not None else
+                                  f"row-shard x{world}" + (
                        (f" + NCCL all-reduce of m x d partials, pipelined over {args.chunks} bucket ranges"
                         if pipelined else " + NCCL all-reduce of m x d partials") if world > 1 else "")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "remeasured": remeasured,
         "build_ms": round(build_ms, 3), "kernel_ms_max_over_ranks": round(kern_ms_max, 4),
     }
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return line if rank == 0 else None
 
@@ -585,6 +598,9 @@ def main():
                          "lowrank: config 5 low-rank error ratio")
     ap.add_argument("--exact", action="store_true",
                     help="bit-exact deterministic kernels also for configs that default to fast mode (c5)")
+    ap.add_argument("--fused", action="store_true",
+                    help="dense, under torchrun: exchange fused into K3 (partial rows pushed to owner ranks over "
+                         "NVLink symmetric memory, owner slot sums, all-gather) instead of the NCCL all-reduce")
     ap.add_argument("--chunks", type=int, default=4,
                     help="N > 1: bucket ranges whose all-reduce overlaps the next range's compute")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -175,6 +175,25 @@ skt_status skt_residual_csr(int64_t n, int64_t d, const void *a_indptr, skt_ityp
                             skt_dtype b_dtype, int64_t ldb, double *out_sq, void *ws,
                             size_t ws_bytes, void *stream);
 
+/* ---- fused exchange for row-sharded multi-GPU S.A ------------------------ */
+/* skt_apply_dense_push: K3 (TMA gather4 kernel; rows of 512 B .. 2 KB) that
+ * stores each partial bucket row straight into its owner rank's receive
+ * buffer instead of a local SA: owner g holds buckets [bounds[g],
+ * bounds[g+1]) (nranks + 1 host int64), peers[g] (host array of nranks
+ * pointers) is g's receive buffer -- a peer pointer over NVLink (symmetric
+ * memory) or local -- laid out [src rank][cap bucket rows][ldr], and this
+ * rank (me) writes slot me.  b0 = global id of local bucket 0 (bucket-range
+ * launches).  skt_slot_sum: out[r][c] = sum over src = 0 .. nslots-1, in that
+ * order, of recv[src * slot_stride + r * ldr + c] (fp64 accumulation) -- the
+ * owner's deterministic reduction after a cross-rank barrier. */
+skt_status skt_apply_dense_push(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                                const void *a, skt_dtype a_dtype, int64_t d, int64_t lda,
+                                skt_dtype out_dtype, void *const *peers, const int64_t *bounds,
+                                int32_t nranks, int32_t me, int64_t cap, int64_t ldr, int64_t b0,
+                                int32_t *nonfinite_flag, void *stream);
+skt_status skt_slot_sum(const void *recv, skt_dtype dtype, int32_t nslots, int64_t rows, int64_t d,
+                        int64_t slot_stride, int64_t ldr, void *out, int64_t ldo, void *stream);
+
 /* ---- passes of the preconditioned iterations and the rank-k residual ----- */
 /* SURVEY §8f rank 2, the passes over original data after the sketch.  M is
  * the n x r row-major fp64 product A R (regress.py:203, r <= 256); y, p are

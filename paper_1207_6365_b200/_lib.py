@@ -38,6 +38,8 @@ EXPORTS = (
     "skt_plan_build",
     "skt_apply_dense",
     "skt_apply_csr",
+    "skt_apply_dense_push",
+    "skt_slot_sum",
     "skt_apply_right_dense",
     "skt_apply_right_csr",
     "skt_lev_rownorms_csr",
@@ -132,6 +134,8 @@ def lib() -> ctypes.CDLL:
         "skt_plan_build": ([P, P, i64, u64, i32, P, P, P, P, sz, P], i32),
         "skt_apply_dense": ([P, P, u64, i64, P, i32, i64, i64, P, i32, i64, P, P], i32),
         "skt_apply_csr": ([P, P, P, i32, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, u32, P], i32),
+        "skt_apply_dense_push": ([P, P, u64, i64, P, i32, i64, i64, i32, P, P, i32, i32, i64, i64, i64, P, P], i32),
+        "skt_slot_sum": ([P, i32, i32, i64, i64, i64, i64, P, i64, P], i32),
         "skt_apply_right_dense": ([P, P, u64, i64, i64, P, i32, i64, P, i32, i64, P, P], i32),
         "skt_apply_right_csr": ([P, P, u64, i64, i64, P, i32, P, i32, P, i32, P, i32, i64, P], i32),
         "skt_lev_rownorms_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, P, i32, P], i32),

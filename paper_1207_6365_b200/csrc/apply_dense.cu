@@ -306,7 +306,7 @@ skt_status dispatch_vec(const int64_t *indptr, const uint32_t *rows, uint64_t t,
                                    : dense_g4_kernel<TIn, TOut, 4, false>;
       SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "skt_apply_dense");
       SKT_LAUNCH(k, (unsigned)blocks, kG4Warps * 32, smem, stream, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
-                 ldsa, flag, (const unsigned char *)a, lda_bytes, 0.0, nbox);
+                 ldsa, flag, (const unsigned char *)a, lda_bytes, 0.0, nbox, PushTable{});
       return check_launch("skt_apply_dense");
     }
   }
@@ -355,4 +355,86 @@ extern "C" skt_status skt_apply_dense(const int64_t *indptr, const uint32_t *row
   return sa_dtype == SKT_F64
              ? dispatch_vec<double, double>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n)
              : dispatch_vec<double, float>(indptr, rows, t, a, d, lda, sa, ldsa, nonfinite_flag, stream, n);
+}
+
+// ---- fused exchange (row-sharded multi-GPU): K3 that pushes partial rows to
+// their owner ranks' receive buffers, and the owner's fixed-order slot sum
+namespace skt {
+namespace {
+template <typename TIn, typename TOut>
+skt_status launch_push(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n, const void *a_,
+                       int64_t d, int64_t lda, const PushTable &pt, int32_t *flag, cudaStream_t stream) {
+  static const char *fn = "skt_apply_dense_push";
+  const TIn *a = (const TIn *)a_;
+  const int64_t row_bytes = d * (int64_t)sizeof(TIn), lda_bytes = lda * (int64_t)sizeof(TIn);
+  const int nbox = g4_boxes(d, (int64_t)sizeof(TIn));
+  CUtensorMap map;
+  if (nbox == 0 || lda_bytes % 16 != 0 || (uintptr_t)a % 16 != 0 || n < 1 || n >= (1LL << 31) ||
+      !make_row_map(&map, a, sizeof(TIn) == 8, n, d, lda_bytes, d / nbox))
+    return fail(SKT_ENOTSUP, fn, "fused push needs rows the gather4 kernel takes (512 B .. 2 KB, 16-byte aligned)");
+  const size_t smem = dense_g4_smem((int)row_bytes);
+  const int64_t blocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
+  auto k = row_bytes == 512    ? dense_g4_kernel<TIn, TOut, 1, true, false, true>
+           : row_bytes == 1024 ? dense_g4_kernel<TIn, TOut, 2, true, false, true>
+           : row_bytes == 2048 ? dense_g4_kernel<TIn, TOut, 4, true, false, true>
+           : row_bytes < 1024  ? dense_g4_kernel<TIn, TOut, 2, false, false, true>
+                               : dense_g4_kernel<TIn, TOut, 4, false, false, true>;
+  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+  SKT_LAUNCH(k, (unsigned)blocks, kG4Warps * 32, smem, stream, map, indptr, rows, t, (int)row_bytes, (int)d,
+             (TOut *)nullptr, (int64_t)0, flag, (const unsigned char *)a, lda_bytes, 0.0, nbox, pt);
+  return check_launch(fn);
+}
+}  // namespace
+}  // namespace skt
+
+extern "C" skt_status skt_apply_dense_push(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                                           const void *a, skt_dtype a_dtype, int64_t d, int64_t lda,
+                                           skt_dtype out_dtype, void *const *peers, const int64_t *bounds,
+                                           int32_t nranks, int32_t me, int64_t cap, int64_t ldr, int64_t b0,
+                                           int32_t *nonfinite_flag, void *stream_) {
+  static const char *fn = "skt_apply_dense_push";
+  if (!indptr || t < 1 || n < 0 || d < 1 || lda < d || !peers || !bounds || nranks < 1 ||
+      nranks > kPushMaxRanks || me < 0 || me >= nranks || cap < 1 || ldr < d || b0 < 0 ||
+      (a_dtype != SKT_F32 && a_dtype != SKT_F64) || (out_dtype != SKT_F32 && out_dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  PushTable pt{};
+  for (int g = 0; g < nranks; ++g) {
+    if (!peers[g] || bounds[g + 1] < bounds[g] || bounds[g + 1] - bounds[g] > cap)
+      return fail(SKT_EINVAL, fn, "bad peer table");
+    pt.peer[g] = peers[g];
+  }
+  for (int g = 0; g <= nranks; ++g) pt.bounds[g] = bounds[g];
+  if (b0 + (int64_t)t > bounds[nranks]) return fail(SKT_EINVAL, fn, "buckets beyond the owner ranges");
+  pt.cap = cap;
+  pt.ldr = ldr;
+  pt.nranks = nranks;
+  pt.me = me;
+  pt.b0 = b0;
+  cudaStream_t stream = as_stream(stream_);
+  if (nonfinite_flag) SKT_CUDA_TRY(cudaMemsetAsync(nonfinite_flag, 0, sizeof(int32_t), stream), fn);
+  if (n > 0 && (!a || !rows)) return fail(SKT_EINVAL, fn, "NULL buffer");
+  if (a_dtype == SKT_F32)
+    return out_dtype == SKT_F64 ? launch_push<float, double>(indptr, rows, t, n, a, d, lda, pt, nonfinite_flag, stream)
+                                : launch_push<float, float>(indptr, rows, t, n, a, d, lda, pt, nonfinite_flag, stream);
+  return out_dtype == SKT_F64 ? launch_push<double, double>(indptr, rows, t, n, a, d, lda, pt, nonfinite_flag, stream)
+                              : launch_push<double, float>(indptr, rows, t, n, a, d, lda, pt, nonfinite_flag, stream);
+}
+
+extern "C" skt_status skt_slot_sum(const void *recv, skt_dtype dtype, int32_t nslots, int64_t rows, int64_t d,
+                                   int64_t slot_stride, int64_t ldr, void *out, int64_t ldo, void *stream_) {
+  static const char *fn = "skt_slot_sum";
+  if (!recv || !out || nslots < 1 || rows < 0 || d < 0 || ldr < d || ldo < d || slot_stride < rows * ldr ||
+      (dtype != SKT_F32 && dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  if (rows == 0 || d == 0) return SKT_OK;
+  const int64_t total = rows * d;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16));
+  cudaStream_t st = as_stream(stream_);
+  if (dtype == SKT_F32)
+    SKT_LAUNCH(slot_sum_kernel<float>, (unsigned)blocks, 256, 0, st, (const float *)recv, nslots, rows, d,
+               slot_stride, ldr, (float *)out, ldo);
+  else
+    SKT_LAUNCH(slot_sum_kernel<double>, (unsigned)blocks, 256, 0, st, (const double *)recv, nslots, rows, d,
+               slot_stride, ldr, (double *)out, ldo);
+  return check_launch(fn);
 }

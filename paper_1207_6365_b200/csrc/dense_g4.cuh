@@ -115,19 +115,35 @@ __device__ bool g4_rescan(const unsigned char *a, int64_t lda_bytes, const int64
   return __any_sync(0xffffffffu, bad);
 }
 
+// Fused exchange (row-sharded multi-GPU S.A): instead of writing its partial
+// bucket row into its own SA, the kernel stores it straight into the owner
+// rank's receive buffer -- a peer pointer over NVLink (symmetric memory) --
+// slot [my_rank][bucket - bounds[owner]], so the transfer overlaps the
+// remaining buckets' compute; the owner then sums its N slots in rank order.
+constexpr int kPushMaxRanks = 8;
+struct PushTable {
+  void *peer[kPushMaxRanks];           // receive buffer base of each rank (device / peer pointers)
+  int64_t bounds[kPushMaxRanks + 1];   // owner g holds buckets [bounds[g], bounds[g + 1])
+  int64_t cap;                         // bucket rows per source slot (>= max owner range)
+  int64_t ldr;                         // row stride of a slot (elements)
+  int nranks, me;
+  int64_t b0;                          // global bucket id of local bucket 0 (bucket-range launches)
+};
+
 // K = 16-byte chunks per lane per row (row_bytes <= K * 512).  A row is fetched
 // as nbox (1 or 2) column boxes of row_bytes / nbox (a box is <= 256 elements,
 // 1 KB); a stage holds box b's four rows at b * 4 * box_bytes.
 // kW: every term weighted by w (the generalized embedding's 1/sqrt(k), with
 // the reference's separate rounding of the product), otherwise w is unused.
-template <typename TIn, typename TOut, int K, bool kFull, bool kW = false>
+template <typename TIn, typename TOut, int K, bool kFull, bool kW = false, bool kPush = false>
 __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const int64_t *__restrict__ indptr,
                                                                  const uint32_t *__restrict__ rows, uint64_t t,
                                                                  int row_bytes, int d, TOut *__restrict__ sa,
                                                                  int64_t ldsa, int32_t *__restrict__ flag,
                                                                  const unsigned char *__restrict__ a_raw,
-                                                                 int64_t lda_bytes, double wgt, int nbox) {
+                                                                 int64_t lda_bytes, double wgt, int nbox,
+                                                                 const __grid_constant__ PushTable push) {
   constexpr int E = G4<TIn>::E;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[kG4Warps][kG4Stages];
@@ -232,6 +248,12 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   }
   bool bad = false;
   TOut *o = sa + bucket * ldsa;
+  if (kPush) {  // the owner rank's receive slot (warp-uniform owner search, <= 8 ranks)
+    const int64_t gb = push.b0 + bucket;
+    int g = 0;
+    while (g + 1 < push.nranks && gb >= push.bounds[g + 1]) ++g;
+    o = (TOut *)push.peer[g] + ((int64_t)push.me * push.cap + (gb - push.bounds[g])) * push.ldr;
+  }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int col = (k * 32 + lane) * E;
@@ -244,6 +266,21 @@ __global__ void __launch_bounds__(kG4Warps * 32) dense_g4_kernel(const __grid_co
   if (flag && __any_sync(0xffffffffu, bad)) {
     const bool real = sizeof(TIn) == 4 || g4_rescan<TIn>(a_raw, lda_bytes, beg, nrows, rows, row_bytes, lane);
     if (real && lane == 0) atomicOr(flag, 1);
+  }
+}
+
+// out[r][c] = sum over src = 0 .. nslots-1 (in that order) of recv[src][r][c]:
+// the owner's fixed-order reduction of the pushed partials (deterministic)
+template <typename T>
+__global__ void __launch_bounds__(256) slot_sum_kernel(const T *__restrict__ recv, int nslots, int64_t rows, int64_t d,
+                                                       int64_t slot_stride, int64_t ldr, T *__restrict__ out,
+                                                       int64_t ldo) {
+  const int64_t total = rows * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i % d;
+    double acc = (double)recv[r * ldr + c];
+    for (int s = 1; s < nslots; ++s) acc += (double)recv[s * slot_stride + r * ldr + c];
+    out[r * ldo + c] = (T)acc;
   }
 }
 

@@ -192,7 +192,7 @@ extern "C" skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t 
       const size_t smem = dense_g4_smem((int)row_bytes);
       const int64_t gblocks = ((int64_t)t + kG4Warps - 1) / kG4Warps;
       typedef void (*KFn)(const CUtensorMap, const int64_t *, const uint32_t *, uint64_t, int, int, double *, int64_t,
-                          int32_t *, const unsigned char *, int64_t, double, int);
+                          int32_t *, const unsigned char *, int64_t, double, int, const PushTable);
 #define SKT_G4W(TIN)                                                                \
   (row_bytes == 512    ? (KFn)dense_g4_kernel<TIN, double, 1, true, true>           \
    : row_bytes == 1024 ? (KFn)dense_g4_kernel<TIN, double, 2, true, true>           \
@@ -203,7 +203,7 @@ extern "C" skt_status skt_gse_apply_dense(const int64_t *indptr, const uint32_t 
 #undef SKT_G4W
       SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
       SKT_LAUNCH(k, (unsigned)gblocks, kG4Warps * 32, smem, st, map, indptr, rows, t, (int)row_bytes, (int)d, sa,
-                 ldsa, nonfinite_flag, (const unsigned char *)a, lda_bytes, weight, nbox);
+                 ldsa, nonfinite_flag, (const unsigned char *)a, lda_bytes, weight, nbox, PushTable{});
       return check_launch(fn);
     }
   }

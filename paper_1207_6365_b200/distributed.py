@@ -14,6 +14,8 @@ collective can be exercised on CPU with the gloo backend in tests.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -152,3 +154,102 @@ class BucketShardedSparseEmbedding:
 
     def descriptor(self) -> dict:
         return {"family": self.family, "n": self.input_dim, "t": self.output_dim, "seed": self.seed}
+
+
+# ---------------------------------------------------------------------------
+# Fused exchange: K3 pushes partial rows into the owner ranks' receive buffers
+# ---------------------------------------------------------------------------
+def owner_bounds(t: int, world: int) -> list[int]:
+    """Owner g of the fused exchange holds buckets [b_g, b_{g+1})."""
+    return [g * t // world for g in range(world + 1)]
+
+
+def _push(op, a_local, out_dtype, peers, bounds, me, cap, ldr):
+    """skt_apply_dense_push for one rank's shard operator ``op``."""
+    from . import _lib
+    from .sketch import _TORCH_TO_SKT, _ptr, _stream_ptr
+
+    n, d = a_local.shape
+    P = ctypes.c_void_p * len(peers)
+    B = ctypes.c_int64 * len(bounds)
+    with torch.cuda.device(a_local.device):
+        _lib.check(_lib.lib().skt_apply_dense_push(
+            _ptr(op.plan_indptr), _ptr(op.plan_rows), op.output_dim, n, _ptr(a_local), _TORCH_TO_SKT[a_local.dtype],
+            d, max(a_local.stride(0), d), _TORCH_TO_SKT[out_dtype], P(*peers), B(*bounds), len(peers), me, cap, ldr,
+            0, None, _stream_ptr(a_local.device)))
+
+
+def _slot_sum(recv, nslots, rows, d, cap, out):
+    from . import _lib
+    from .sketch import _TORCH_TO_SKT, _ptr, _stream_ptr
+
+    with torch.cuda.device(recv.device):
+        _lib.check(_lib.lib().skt_slot_sum(_ptr(recv), _TORCH_TO_SKT[recv.dtype], nslots, rows, d, cap * d, d,
+                                           _ptr(out), d, _stream_ptr(recv.device)))
+
+
+def fused_apply_emulated(ops, a_shards, out_dtype=torch.float64):
+    """The fused exchange with all ranks' data on ONE device (the way to test
+    it with one GPU: the ranks never wait on one another -- every push lands in
+    a local buffer, then every owner sums its slots): returns the full t x d SA.
+    ``ops[g]`` is rank g's shard operator, ``a_shards[g]`` its rows."""
+    world = len(ops)
+    t, d = ops[0].output_dim, a_shards[0].shape[1]
+    bounds = owner_bounds(t, world)
+    cap = max(bounds[g + 1] - bounds[g] for g in range(world))
+    dev = a_shards[0].device
+    recv = [torch.zeros((world * cap, d), dtype=out_dtype, device=dev) for _ in range(world)]
+    peers = [r.data_ptr() for r in recv]
+    for g, (op, a) in enumerate(zip(ops, a_shards)):
+        _push(op, a, out_dtype, peers, bounds, g, cap, d)
+    out = torch.empty((t, d), dtype=out_dtype, device=dev)
+    for g in range(world):
+        rows = bounds[g + 1] - bounds[g]
+        if rows:
+            _slot_sum(recv[g], world, rows, d, cap, out[bounds[g]:bounds[g + 1]])
+    return out
+
+
+class FusedShardedSparseEmbedding(ShardedSparseEmbedding):
+    """Row-sharded S.A whose exchange is fused into K3: each rank's kernel
+    stores its partial bucket rows straight into the owner rank's receive
+    buffer over NVLink (torch symmetric memory: every rank maps every other
+    rank's buffer), so the transfer overlaps the compute of the remaining
+    buckets; after a cross-rank barrier each owner sums its N slots in rank
+    order (deterministic) and the SA row blocks are all-gathered (NCCL).
+    Dense input with rows the gather4 kernel takes (512 B .. 2 KB).  The data
+    path is tested on one GPU by fused_apply_emulated; the symmetric-memory
+    plumbing needs >= 2 GPUs (bench.py --fused)."""
+
+    def __init__(self, n, t, seed, group=None, device=None):
+        super().__init__(n, t, seed, group=group, device=device)
+        self.bounds = owner_bounds(self.output_dim, self.world)
+        self.cap = max(self.bounds[g + 1] - self.bounds[g] for g in range(self.world))
+        self._bufs = {}
+
+    def _buffers(self, d, dtype, device):
+        key = (d, dtype)
+        if key not in self._bufs:
+            import torch.distributed._symmetric_memory as symm_mem
+
+            recv = symm_mem.empty((self.world * self.cap, d), dtype=dtype, device=device)
+            hdl = symm_mem.rendezvous(recv, group=self.group if self.group is not None else dist.group.WORLD)
+            peers = [hdl.get_buffer(g, (self.world * self.cap, d), dtype).data_ptr() for g in range(self.world)]
+            self._bufs[key] = (recv, hdl, peers)
+        return self._bufs[key]
+
+    def apply(self, a_local, out_dtype=torch.float64, async_op: bool = False, chunks: int = 1):
+        d = a_local.shape[1]
+        recv, hdl, peers = self._buffers(d, out_dtype, a_local.device)
+        hdl.barrier()  # every owner has summed the previous apply's slots
+        _push(self.local, a_local, out_dtype, peers, self.bounds, self.rank, self.cap, d)
+        hdl.barrier()  # every rank's pushes have landed
+        block = torch.empty((self.cap, d), dtype=out_dtype, device=a_local.device)
+        mine = self.bounds[self.rank + 1] - self.bounds[self.rank]
+        if mine:
+            _slot_sum(recv, self.world, mine, d, self.cap, block[:mine])
+        gathered = torch.empty((self.world * self.cap, d), dtype=out_dtype, device=a_local.device)
+        dist.all_gather_into_tensor(gathered, block, group=self.group)
+        out = torch.cat([gathered[g * self.cap: g * self.cap + self.bounds[g + 1] - self.bounds[g]]
+                         for g in range(self.world)])
+        return out
