@@ -38,6 +38,9 @@ inline size_t lev_tc3_smem(int dk, int k) {  // A: 128 x dk words; B: 2k x 2dk f
 #ifndef SKT_TC3_BLOCKCLEAR
 #define SKT_TC3_BLOCKCLEAR 1
 #endif
+#ifndef SKT_TC3_L2PF
+#define SKT_TC3_L2PF 1
+#endif
 
 template <typename IP, typename IX, typename TS>
 __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d, int dk,
@@ -306,6 +309,14 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
     len_c = len_n;
     rs_n = (int64_t)rb_2;
     len_n = (int)((int64_t)re_2 - (int64_t)rb_2);
+#if SKT_TC3_L2PF
+    // tile + 2's rows into L2 now: its register loads (issued one iteration
+    // from here, consumed right after this tile's epilogue) then hit L2
+    if (len_n > 0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(aix + rs_n));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(av + rs_n));
+    }
+#endif
     load_desc_raw(tile + 3 * (int64_t)gridDim.x, rb_2, re_2);
     // ---- wait for the accumulator
     asm volatile(
