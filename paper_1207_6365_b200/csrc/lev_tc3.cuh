@@ -316,6 +316,10 @@ __global__ void __launch_bounds__(kTcThreads, 4) lev_tc3_kernel(int64_t n, int d
       asm volatile("prefetch.global.L2 [%0];" ::"l"(aix + rs_n));
       asm volatile("prefetch.global.L2 [%0];" ::"l"(av + rs_n));
     }
+    if (len_n > 24) {  // long rows: their next 128 bytes too
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(aix + rs_n + 32));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(av + rs_n + 32));
+    }
 #endif
     load_desc_raw(tile + 3 * (int64_t)gridDim.x, rb_2, re_2);
     // ---- wait for the accumulator
