@@ -23,7 +23,8 @@ def main():
         op = SparseEmbedding(n, t, seed=7)
         h, s = O.hash_signs(n, t, 7)
         assert np.array_equal(op.bucket, h.astype(np.int64))
-        for d, dt in [(1, np.float64), (20, np.float64), (128, np.float32), (256, np.float32), (33, np.float32)]:
+        for d, dt in [(1, np.float64), (20, np.float64), (128, np.float32), (256, np.float32), (33, np.float32),
+                      (200, np.float32), (384, np.float32), (64, np.float64), (256, np.float64)]:  # gather4 rows
             a = rng.standard_normal((n, d)).astype(dt)
             assert np.array_equal(op.apply(a), O.apply_dense(h, s, t, a))
             checks += 1
@@ -58,6 +59,27 @@ def main():
     got64 = lev_rownorms(sp.csr_array(a32, dtype=np.float64), probe)
     assert np.max(np.abs(got64 - ref) / ref) <= 1e-12
     checks += 4
+    # the passes after the sketch and the fused exchange
+    from paper_1207_6365_b200 import cgnr_solve, precondition, richardson_solve
+    from paper_1207_6365_b200.distributed import fused_apply_emulated, shard_rows
+    from paper_1207_6365_b200.lowrank import _residual_norm
+
+    am = rng.standard_normal((4000, 6))
+    bm = am @ rng.standard_normal((6, 1)) + 0.01 * rng.standard_normal((4000, 1))
+    pre = precondition(am, 0.5, seed=1)
+    for fn in (richardson_solve, cgnr_solve):
+        sol = fn(am, pre, bm, 1e-6, max_iter=20)
+        assert sol.residual_norm <= 1.01 * np.linalg.norm(am @ np.linalg.lstsq(am, bm, rcond=None)[0] - bm)
+    sa_ = sp.csr_array(sp.random_array((2100, 2000), density=0.01, rng=rng, format="csr"))
+    lq, _ = np.linalg.qr(rng.standard_normal((2100, 3)))
+    wq, _ = np.linalg.qr(rng.standard_normal((2000, 3)))
+    _residual_norm(sa_, lq, np.ones(3), wq)
+    at = torch.from_numpy(rng.standard_normal((3001, 128)).astype(np.float32)).cuda()
+    ops = [SparseEmbedding(3001, 37, 2, row_range=shard_rows(3001, 3, g)) for g in range(3)]
+    shards = [at[slice(*shard_rows(3001, 3, g))].contiguous() for g in range(3)]
+    full = SparseEmbedding(3001, 37, 2).apply(at)
+    assert float((fused_apply_emulated(ops, shards) - full).norm() / full.norm()) <= 1e-12
+    checks += 5
     torch.cuda.synchronize()
     print(f"sanitize cases ok: {checks} checks")
 
