@@ -80,3 +80,36 @@ def test_shim_rebinds_reference_module_globals():
         skb.uninstall()
     assert ref.SparseEmbedding is orig
     assert ref.SrhtOperator is not skb.SrhtOperator
+
+
+def test_srht_dims_and_nnls_match_reference():
+    """Host pieces of the callers against the reference itself (build
+    container; skipped where the reference is absent): default_srht_dim
+    (sketch.py:83-94) and Lawson-Hanson NNLS (regress.py:288-327) -- the same
+    numpy operations, so the same bits."""
+    ref_sketch = pytest.importorskip("sketchnla.sketch")
+    ref_regress = importlib.import_module("sketchnla.regress")
+    from paper_1207_6365_b200.solvers import default_srht_dim, lawson_hanson_nnls
+
+    for r in (1, 5, 12, 30):
+        for eps in (0.1, 1 / 6, 0.25, 0.5):
+            for n in (100, 8920, 10**6):
+                assert default_srht_dim(r, eps, n) == ref_sketch.default_srht_dim(r, eps, n)
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        m = rng.standard_normal((60, 7))
+        y = m @ rng.standard_normal(7) + 0.1 * rng.standard_normal(60)
+        assert np.array_equal(lawson_hanson_nnls(m, y), ref_regress.lawson_hanson_nnls(m, y))
+
+
+def test_fused_exchange_owner_layout():
+    """Owner ranges of the fused exchange cover the buckets once; every
+    rank's slot fits the receive buffer."""
+    from paper_1207_6365_b200.distributed import owner_bounds
+
+    for t in (1, 7, 1001, 65536):
+        for world in (1, 2, 3, 8):
+            b = owner_bounds(t, world)
+            assert b[0] == 0 and b[-1] == t and all(b[g] <= b[g + 1] for g in range(world))
+            cap = max(b[g + 1] - b[g] for g in range(world))
+            assert cap * world >= t and cap <= -(-t // world)
