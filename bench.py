@@ -132,6 +132,24 @@ def gather_ceiling_ms(cfg_name: str):
         return None
 
 
+def dominant_kernel(cfg, lev: bool, args, sa_dt) -> str:
+    """Name of the kernel the line's roofline describes (the library picks it by
+    shape)."""
+    if lev:
+        return "lev_tc3_kernel (tcgen05 kind::f16, scaled 2xFP16)"
+    if cfg["kind"] == "dense":
+        esz = 4 if cfg["dtype"] == "f32" else 8
+        rb = cfg["d"] * esz
+        if 512 <= rb <= 2048 and rb % 16 == 0 and os.environ.get("SKT_DENSE_G4", "1") != "0":
+            return "dense_g4_kernel (TMA tile::gather4 into an mbarrier smem ring)"
+        return "apply_dense_kernel (register gather)"
+    if cfg.get("fast") and not args.exact:
+        return "csr_atomic_kernel (fast mode: unordered RED.ADD)"
+    if cfg["d"] > 256:
+        return "csr_rowseq_block_kernel (deterministic wide-d)"
+    return "csr_group_kernel (grouped sweep)" if cfg.get("per_row", 16) <= 8 else "csr_tile_kernel (densify tiles)"
+
+
 def traffic_for(cfg_name: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/ncu_traffic.json), or None."""
@@ -515,7 +533,8 @@ def our_arm(args, cfg):
                 "frac": round(achieved / peak, 4), "traffic": traffic_for(args.config if lev is None else args.config + "_lev"),
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs copy bandwidth)",
                 "kernel_ms": round(kern_ms, 4), "alg_bytes_per_launch": alg_bytes,
-                "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}
+                "frac_of_8TBps_nominal": round(achieved / 8000.0, 4),
+                "kernel": dominant_kernel(cfg, lev is not None, args, sa_dt)}
     gc = gather_ceiling_ms(args.config) if (cfg["kind"] == "csr" and lev is None and world == 1) else None
     if gc is not None:
         # CSR S.A reads every row's (indptr pair, index segment, value segment)
