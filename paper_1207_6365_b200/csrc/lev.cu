@@ -104,6 +104,53 @@ __global__ void __launch_bounds__(kThreads) lev_csr_kernel(
   }
 }
 
+// k == 32, probe in shared memory: a HALF warp per row, lane owns columns
+// 2l', 2l'+1 (one 16-byte probe load per entry); the two rows of a warp share
+// every shuffle, so the shared-memory pipe does about half the work per entry
+// of the warp-per-row kernel.  Per score the order of the fp64 FMAs over a
+// row's entries is the same (ascending entries), per column pair.
+template <typename IP, typename IX, typename TV, typename TS>
+__global__ void __launch_bounds__(kThreads) lev_csr_k32_kernel(int64_t n, int64_t d, const IP *__restrict__ aip,
+                                                               const IX *__restrict__ aix, const TV *__restrict__ av,
+                                                               const double *__restrict__ probe,
+                                                               TS *__restrict__ scores) {
+  extern __shared__ __align__(16) double sprobe[];
+  for (int64_t i = threadIdx.x; i < d * 32; i += blockDim.x) sprobe[i] = probe[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+  const double2 *sp2 = reinterpret_cast<const double2 *>(sprobe);
+  for (int64_t r0 = 2 * warp; r0 < n; r0 += 2 * nwarps) {
+    const int64_t row = r0 + half;
+    const bool live = row < n;
+    const int64_t rs = live ? (int64_t)aip[row] : 0, re = live ? (int64_t)aip[row + 1] : 0;
+    const int len = (int)(re - rs);
+    const int lmax = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
+    double a0 = 0.0, a1 = 0.0;
+    for (int p0 = 0; p0 < lmax; p0 += 16) {
+      const int p = p0 + hl;
+      const bool has = p < len;
+      const int32_t j = has ? (int32_t)aix[rs + p] : 0;
+      const double v = has ? (double)av[rs + p] : 0.0;
+      const int cnt = min(16, lmax - p0);
+      for (int q = 0; q < cnt; ++q) {
+        const int32_t jq = __shfl_sync(0xffffffffu, j, q, 16);
+        const double vq = __shfl_sync(0xffffffffu, v, q, 16);
+        if (p0 + q < len) {  // this half's row still has entry p0 + q
+          const double2 pr = sp2[(int64_t)jq * 16 + hl];
+          a0 = fma(vq, pr.x, a0);
+          a1 = fma(vq, pr.y, a1);
+        }
+      }
+    }
+    double sc = fma(a0, a0, a1 * a1);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    if (live && hl == 0) scores[row] = (TS)sc;
+  }
+}
+
 template <typename TA, typename TS, bool kSmemProbe>
 __global__ void __launch_bounds__(kThreads) lev_dense_kernel(int64_t n, int64_t d,
                                                              const TA *__restrict__ a, int64_t lda,
@@ -197,6 +244,17 @@ skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, co
   }
   const size_t pbytes = (size_t)d * k * sizeof(double);
   const int64_t blocks = grid_for(n);
+  static const bool k32 = [] {
+    const char *e = getenv("SKT_LEV_K32");
+    return !(e && e[0] == '0');
+  }();
+  if (k == 32 && k32 && pbytes <= kProbeSmemMax) {
+    auto kern = lev_csr_k32_kernel<IP, IX, TV, TS>;
+    SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes), fn);
+    SKT_LAUNCH(kern, (unsigned)blocks, kThreads, pbytes, st, n, d, (const IP *)aip, (const IX *)aix, (const TV *)av, p,
+               (TS *)scores);
+    return check_launch(fn);
+  }
   if (pbytes <= kProbeSmemMax) {
     auto kern = lev_csr_kernel<IP, IX, TV, TS, true>;
     SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes), fn);
