@@ -104,49 +104,62 @@ __global__ void __launch_bounds__(kThreads) lev_csr_kernel(
   }
 }
 
-// k == 32, probe in shared memory: a HALF warp per row, lane owns columns
-// 2l', 2l'+1 (one 16-byte probe load per entry); the two rows of a warp share
-// every shuffle, so the shared-memory pipe does about half the work per entry
-// of the warp-per-row kernel.  Per score the order of the fp64 FMAs over a
-// row's entries is the same (ascending entries), per column pair.
-template <typename IP, typename IX, typename TV, typename TS>
+// k == 32, probe in shared memory: a HALF warp per row (LPR = 16), lane owns
+// columns 2l', 2l'+1 (one 16-byte probe load per entry); the two rows of a
+// warp share every shuffle, so the shared-memory pipe does about half the work
+// per entry of the warp-per-row kernel (config 4 shape, fp64: 2.0 -> 1.33 ms).
+// Per score the order of the fp64 FMAs over a row's entries is the same
+// (ascending entries), per column.
+template <typename IP, typename IX, typename TV, typename TS, int LPR>
 __global__ void __launch_bounds__(kThreads) lev_csr_k32_kernel(int64_t n, int64_t d, const IP *__restrict__ aip,
                                                                const IX *__restrict__ aix, const TV *__restrict__ av,
                                                                const double *__restrict__ probe,
                                                                TS *__restrict__ scores) {
+  // LPR lanes per row (16 or 8), CPL = 32 / LPR columns per lane, 32 / LPR
+  // rows per warp sharing every shuffle
+  constexpr int CPL = 32 / LPR, RPW = 32 / LPR, V2 = CPL / 2;
   extern __shared__ __align__(16) double sprobe[];
   for (int64_t i = threadIdx.x; i < d * 32; i += blockDim.x) sprobe[i] = probe[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, hl = lane % LPR;
   const int64_t warp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
   const double2 *sp2 = reinterpret_cast<const double2 *>(sprobe);
-  for (int64_t r0 = 2 * warp; r0 < n; r0 += 2 * nwarps) {
-    const int64_t row = r0 + half;
+  for (int64_t r0 = RPW * warp; r0 < n; r0 += RPW * nwarps) {
+    const int64_t row = r0 + sub;
     const bool live = row < n;
     const int64_t rs = live ? (int64_t)aip[row] : 0, re = live ? (int64_t)aip[row + 1] : 0;
     const int len = (int)(re - rs);
-    const int lmax = max(len, __shfl_xor_sync(0xffffffffu, len, 16));
-    double a0 = 0.0, a1 = 0.0;
-    for (int p0 = 0; p0 < lmax; p0 += 16) {
+    int lmax = len;
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    double a[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) a[c] = 0.0;
+    for (int p0 = 0; p0 < lmax; p0 += LPR) {
       const int p = p0 + hl;
       const bool has = p < len;
       const int32_t j = has ? (int32_t)aix[rs + p] : 0;
       const double v = has ? (double)av[rs + p] : 0.0;
-      const int cnt = min(16, lmax - p0);
+      const int cnt = min(LPR, lmax - p0);
       for (int q = 0; q < cnt; ++q) {
-        const int32_t jq = __shfl_sync(0xffffffffu, j, q, 16);
-        const double vq = __shfl_sync(0xffffffffu, v, q, 16);
-        if (p0 + q < len) {  // this half's row still has entry p0 + q
-          const double2 pr = sp2[(int64_t)jq * 16 + hl];
-          a0 = fma(vq, pr.x, a0);
-          a1 = fma(vq, pr.y, a1);
+        const int32_t jq = __shfl_sync(0xffffffffu, j, q, LPR);
+        const double vq = __shfl_sync(0xffffffffu, v, q, LPR);
+        if (p0 + q < len) {  // this row still has entry p0 + q
+#pragma unroll
+          for (int h = 0; h < V2; ++h) {
+            const double2 pr = sp2[(int64_t)jq * 16 + hl * V2 + h];
+            a[2 * h] = fma(vq, pr.x, a[2 * h]);
+            a[2 * h + 1] = fma(vq, pr.y, a[2 * h + 1]);
+          }
         }
       }
     }
-    double sc = fma(a0, a0, a1 * a1);
+    double sc = 0.0;
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    for (int c = 0; c < CPL; ++c) sc = fma(a[c], a[c], sc);
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
     if (live && hl == 0) scores[row] = (TS)sc;
   }
 }
@@ -249,7 +262,11 @@ skt_status launch_csr(int64_t n, int64_t d, const void *aip, const void *aix, co
     return !(e && e[0] == '0');
   }();
   if (k == 32 && k32 && pbytes <= kProbeSmemMax) {
-    auto kern = lev_csr_k32_kernel<IP, IX, TV, TS>;
+    static const int lpr = [] {  // lanes per row: 16 (default) or 8 (A/B; measured 8% slower)
+      const char *e = getenv("SKT_LEV_K32_LPR");
+      return e && atoi(e) == 8 ? 8 : 16;
+    }();
+    auto kern = lpr == 16 ? lev_csr_k32_kernel<IP, IX, TV, TS, 16> : lev_csr_k32_kernel<IP, IX, TV, TS, 8>;
     SKT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes), fn);
     SKT_LAUNCH(kern, (unsigned)blocks, kThreads, pbytes, st, n, d, (const IP *)aip, (const IX *)aix, (const TV *)av, p,
                (TS *)scores);
