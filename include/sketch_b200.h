@@ -284,7 +284,9 @@ skt_status skt_gse_apply_csr(const int64_t *indptr, const uint32_t *rows, uint64
  * skt_coo_to_csr canonicalises on the device (io.py:101-102 -> as_csr,
  * _validation.py:30-41): (row, col)-sorted, duplicates summed in file order,
  * zero sums dropped; indptr (n_rows + 1, int64), indices (int32), values
- * (fp64, capacity count), *nnz (device int64). */
+ * (fp64, capacity count), *nnz (device int64); *nonfinite (device int32,
+ * may be NULL) is set to 1 when a kept (summed) entry is NaN or +-inf -- the
+ * caller raises as_csr's "contains non-finite entries" (_validation.py:39-40). */
 typedef struct skt_mm_info {
   int64_t n_rows, n_cols, n_entries;
   int32_t field;     /* 0 real, 1 integer, 2 pattern */
@@ -296,7 +298,7 @@ skt_status skt_mm_read_coo(const char *path, int64_t capacity, int64_t *rows, in
 skt_status skt_coo_to_csr_workspace(int64_t count, int64_t n_rows, int64_t n_cols, size_t *bytes);
 skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, const double *vals, int64_t count,
                           int64_t n_rows, int64_t n_cols, int64_t *indptr, int32_t *indices, double *out_vals,
-                          int64_t *nnz, void *ws, size_t ws_bytes, void *stream);
+                          int64_t *nnz, int32_t *nonfinite, void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

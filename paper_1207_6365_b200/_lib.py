@@ -159,7 +159,7 @@ def lib() -> ctypes.CDLL:
         "skt_mm_probe": ([ctypes.c_char_p, ctypes.POINTER(SktMmInfo)], i32),
         "skt_mm_read_coo": ([ctypes.c_char_p, i64, P, P, P, ctypes.POINTER(i64), i32], i32),
         "skt_coo_to_csr_workspace": ([i64, i64, i64, ctypes.POINTER(sz)], i32),
-        "skt_coo_to_csr": ([P, P, P, i64, i64, i64, P, P, P, P, P, sz, P], i32),
+        "skt_coo_to_csr": ([P, P, P, i64, i64, i64, P, P, P, P, P, P, sz, P], i32),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

@@ -4,7 +4,8 @@
 // sorted column indices).  Entries are ordered by (row, col) with two stable
 // passes of the plan builder K2 (by column, then by row: ties keep file
 // order), duplicate runs are summed in file order, entries whose sum is 0 are
-// dropped, and indptr comes from an integer row histogram + the device scan.
+// dropped, and indptr comes from an integer row histogram + the device scan;
+// a non-finite kept sum raises the caller's flag (as_csr's finiteness check).
 // Deterministic (integer atomics only).
 #include "common.cuh"
 #include "scan.cuh"
@@ -35,7 +36,7 @@ __global__ void coo_order_kernel(const uint32_t *__restrict__ p1, const uint32_t
 __global__ void coo_runs_kernel(const uint32_t *__restrict__ ord, const uint32_t *__restrict__ rs,
                                 const uint32_t *__restrict__ cs, const double *__restrict__ vals, int64_t count,
                                 double *__restrict__ sums, uint32_t *__restrict__ keep,
-                                uint32_t *__restrict__ rowcnt) {
+                                uint32_t *__restrict__ rowcnt, int32_t *__restrict__ nonfinite) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
     const bool head = e == 0 || rs[e] != rs[e - 1] || cs[e] != cs[e - 1];
     uint32_t k = 0;
@@ -43,8 +44,10 @@ __global__ void coo_runs_kernel(const uint32_t *__restrict__ ord, const uint32_t
       double s = vals[ord[e]];
       for (int64_t f = e + 1; f < count && rs[f] == rs[e] && cs[f] == cs[e]; ++f) s += vals[ord[f]];
       sums[e] = s;
-      k = s != 0.0;
+      k = s != 0.0;  // NaN and inf sums are kept, as eliminate_zeros keeps them
       if (k) atomicAdd(rowcnt + rs[e], 1u);
+      // as_csr's finiteness check on the canonical data (_validation.py:39-40)
+      if (nonfinite && !isfinite(s)) atomicOr(nonfinite, 1);
     }
     keep[e] = k;
   }
@@ -131,7 +134,8 @@ extern "C" skt_status skt_coo_to_csr_workspace(int64_t count, int64_t n_rows, in
 
 extern "C" skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, const double *vals, int64_t count,
                                      int64_t n_rows, int64_t n_cols, int64_t *indptr, int32_t *indices,
-                                     double *out_vals, int64_t *nnz, void *ws, size_t ws_bytes, void *stream_) {
+                                     double *out_vals, int64_t *nnz, int32_t *nonfinite, void *ws, size_t ws_bytes,
+                                     void *stream_) {
   static const char *fn = "skt_coo_to_csr";
   if (count < 0 || n_rows < 0 || n_cols < 0 || count >= (1LL << 31) || n_rows >= (1LL << 32) ||
       n_cols >= (1LL << 31) || !indptr || !nnz || (count > 0 && (!rows || !cols || !vals || !indices || !out_vals)))
@@ -141,6 +145,7 @@ extern "C" skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, c
   CooWs w = carve((unsigned char *)ws, count, n_rows, n_cols, pn);
   if (!ws || ws_bytes < w.total) return fail(SKT_EWORKSPACE, fn, "workspace too small");
   SKT_CUDA_TRY(cudaMemsetAsync(w.rowcnt, 0, (n_rows + 1) * 4, st), fn);
+  if (nonfinite) SKT_CUDA_TRY(cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), st), fn);
   if (count > 0 && n_rows > 0 && n_cols > 0) {
     // (1) stable sort by column, (2) stable sort by row -> (row, col) order, ties in file order
     SKT_LAUNCH(coo_keys_kernel, gridn(count), 256, 0, st, cols, (const uint32_t *)nullptr, count, w.keys, w.zero);
@@ -151,7 +156,8 @@ extern "C" skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, c
     s = skt_plan_build(w.keys, w.zero, count, (uint64_t)n_rows, 0, w.pind, w.p2, nullptr, w.plan_ws, w.plan_bytes, st);
     if (s != SKT_OK) return s;
     SKT_LAUNCH(coo_order_kernel, gridn(count), 256, 0, st, w.p1, w.p2, count, rows, cols, w.ord, w.rs, w.cs);
-    SKT_LAUNCH(coo_runs_kernel, gridn(count), 256, 0, st, w.ord, w.rs, w.cs, vals, count, w.sums, w.keep, w.rowcnt);
+    SKT_LAUNCH(coo_runs_kernel, gridn(count), 256, 0, st, w.ord, w.rs, w.cs, vals, count, w.sums, w.keep, w.rowcnt,
+               nonfinite);
     SKT_CUDA_TRY(cudaMemcpyAsync(w.keep_scan, w.keep, count * 4, cudaMemcpyDeviceToDevice, st), fn);
     s = exclusive_scan_u32(w.keep_scan, count, w.part, st, fn);
     if (s != SKT_OK) return s;

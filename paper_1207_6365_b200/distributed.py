@@ -46,12 +46,14 @@ class ShardedSparseEmbedding:
             partial_fn = self._gpu_partial
         self.partial_fn = partial_fn
 
-    def _gpu_partial(self, a_local, out_dtype, buckets=None, out=None):
+    def _gpu_partial(self, a_local, out_dtype, buckets=None, out=None, flag=None):
         if buckets is None:
             return self.local.apply(a_local, out_dtype=out_dtype)
         if out is None:
             out = torch.empty((self.output_dim, a_local.shape[1]), dtype=out_dtype, device=a_local.device)
-        self.local._apply_dense_device(a_local, out_dtype, check_finite=False, out=out, buckets=buckets)
+        # the fused non-finite scan lands in ``flag`` (no host sync inside the
+        # pipeline); apply() checks every range's flag once at the end
+        self.local._apply_dense_device(a_local, out_dtype, out=out, buckets=buckets, flag=flag)
         return out[buckets[0] : buckets[1]]
 
     def bucket_chunks(self, chunks: int):
@@ -77,16 +79,24 @@ class ShardedSparseEmbedding:
             return (part, work) if async_op else part
         device = a_local.device if isinstance(a_local, torch.Tensor) else torch.device("cpu")
         out = torch.empty((self.output_dim, a_local.shape[1]), dtype=out_dtype, device=device)
+        ranges = self.bucket_chunks(chunks)
+        flags = torch.zeros(len(ranges), dtype=torch.int32, device=device)
         works = []
-        for b0, b1 in self.bucket_chunks(chunks):
-            piece = self.partial_fn(a_local, out_dtype, buckets=(b0, b1), out=out)
+        for k, (b0, b1) in enumerate(ranges):
+            piece = self.partial_fn(a_local, out_dtype, buckets=(b0, b1), out=out, flag=flags[k:k + 1])
             if piece.data_ptr() != out[b0:b1].data_ptr():
                 out[b0:b1].copy_(piece)
             works.append(dist.all_reduce(out[b0:b1], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        # non-finite input on any rank raises on every rank (as_dense,
+        # _validation.py:25-26), checked once after the pipeline is issued
+        bad = flags.amax().reshape(1)
+        works.append(dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=self.group, async_op=True))
         if async_op:
             return out, works
         for w in works:
             w.wait()
+        if int(bad.item()) != 0:
+            raise ValueError("matrix contains non-finite entries")
         return out
 
     def descriptor(self) -> dict:
@@ -124,12 +134,16 @@ class BucketShardedSparseEmbedding:
             block_fn = self._gpu_block
         self.block_fn = block_fn
 
-    def _gpu_block(self, a, out_dtype, buckets, deterministic=True):
+    def _gpu_block(self, a, out_dtype, buckets, deterministic=True, canonical=False):
+        """``canonical=True`` asserts that no row of a sparse CSR ``a`` repeats
+        a column (as_csr output, _validation.py:30-41) and unlocks the faster
+        canonical kernels; torch CSR tensors carry no such guarantee, so the
+        default serialises duplicates like SparseEmbedding.apply does."""
         b0, b1 = buckets
         op = self.local
         if isinstance(a, torch.Tensor) and a.layout == torch.sparse_csr:
             ip, ix, vv = (x.to(op.device) for x in (a.crow_indices(), a.col_indices(), a.values()))
-            out = op._apply_csr_device(ip, ix, vv, a.shape[1], out_dtype, canonical=True,
+            out = op._apply_csr_device(ip, ix, vv, a.shape[1], out_dtype, canonical=canonical,
                                        deterministic=deterministic, buckets=buckets)
         else:
             x = a.to(op.device)
@@ -164,19 +178,21 @@ def owner_bounds(t: int, world: int) -> list[int]:
     return [g * t // world for g in range(world + 1)]
 
 
-def _push(op, a_local, out_dtype, peers, bounds, me, cap, ldr):
-    """skt_apply_dense_push for one rank's shard operator ``op``."""
+def _push(op, a_local, out_dtype, peers, bounds, me, cap, ldr, flag=None):
+    """skt_apply_dense_push for one rank's shard operator ``op``; the fused
+    non-finite scan lands in ``flag`` (1-element int32 device tensor)."""
     from . import _lib
-    from .sketch import _TORCH_TO_SKT, _ptr, _stream_ptr
+    from .sketch import _TORCH_TO_SKT, _ptr, _stream_ptr, dense_operand
 
+    a_local = dense_operand(a_local)
     n, d = a_local.shape
     P = ctypes.c_void_p * len(peers)
     B = ctypes.c_int64 * len(bounds)
     with torch.cuda.device(a_local.device):
         _lib.check(_lib.lib().skt_apply_dense_push(
             _ptr(op.plan_indptr), _ptr(op.plan_rows), op.output_dim, n, _ptr(a_local), _TORCH_TO_SKT[a_local.dtype],
-            d, max(a_local.stride(0), d), _TORCH_TO_SKT[out_dtype], P(*peers), B(*bounds), len(peers), me, cap, ldr,
-            0, None, _stream_ptr(a_local.device)))
+            d, max(a_local.stride(0), d, 1) if n > 1 else max(d, 1), _TORCH_TO_SKT[out_dtype], P(*peers),
+            B(*bounds), len(peers), me, cap, ldr, 0, _ptr(flag), _stream_ptr(a_local.device)))
 
 
 def _slot_sum(recv, nslots, rows, d, cap, out):
@@ -238,11 +254,25 @@ class FusedShardedSparseEmbedding(ShardedSparseEmbedding):
             self._bufs[key] = (recv, hdl, peers)
         return self._bufs[key]
 
-    def apply(self, a_local, out_dtype=torch.float64, async_op: bool = False, chunks: int = 1):
+    def apply(self, a_local, out_dtype=torch.float64, async_op: bool = False, chunks: int = 1,
+              check_finite: bool = True):
+        """Same contract as ShardedSparseEmbedding.apply: ``a_local`` holds this
+        rank's rows, non-finite input on any rank raises ValueError on every
+        rank (after the exchange, one flag all-reduce)."""
+        if not isinstance(a_local, torch.Tensor) or not a_local.is_cuda:
+            raise ValueError("the fused exchange takes this rank's rows as a CUDA tensor")
+        if a_local.shape[0] != self.row_end - self.row_begin:
+            raise ValueError(
+                f"rank {self.rank} expects rows [{self.row_begin}, {self.row_end}), got {a_local.shape[0]} rows"
+            )
+        from .sketch import dense_operand
+
+        a_local = dense_operand(a_local)
         d = a_local.shape[1]
         recv, hdl, peers = self._buffers(d, out_dtype, a_local.device)
+        flag = torch.zeros(1, dtype=torch.int32, device=a_local.device) if check_finite else None
         hdl.barrier()  # every owner has summed the previous apply's slots
-        _push(self.local, a_local, out_dtype, peers, self.bounds, self.rank, self.cap, d)
+        _push(self.local, a_local, out_dtype, peers, self.bounds, self.rank, self.cap, d, flag)
         hdl.barrier()  # every rank's pushes have landed
         block = torch.empty((self.cap, d), dtype=out_dtype, device=a_local.device)
         mine = self.bounds[self.rank + 1] - self.bounds[self.rank]
@@ -252,4 +282,8 @@ class FusedShardedSparseEmbedding(ShardedSparseEmbedding):
         dist.all_gather_into_tensor(gathered, block, group=self.group)
         out = torch.cat([gathered[g * self.cap: g * self.cap + self.bounds[g + 1] - self.bounds[g]]
                          for g in range(self.world)])
+        if flag is not None:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+            if int(flag.item()) != 0:
+                raise ValueError("matrix contains non-finite entries")
         return out

@@ -129,20 +129,19 @@ def low_rank_approx(a, k: int, eps: float, seed: int = 0, strategy: str = "srht_
     """lowrank.py:111-222.  The default strategy ("srht_compose": SRHT o sparse
     embedding for both sketches) and explicit sparse-embedding sketches run
     here with every sketch on the GPU; "leverage_sample" (leverage-score row
-    samplers, another sketch family) is handed to the reference package when
-    it is importable."""
+    samplers, another sketch family) raises -- this package never runs the
+    reference's CPU code."""
     if strategy not in STRATEGIES:
         raise ValueError(f"strategy must be one of {STRATEGIES}, got {strategy!r}")
     if strategy != "srht_compose" and (r_op is None or s_op is None):
-        try:
-            from sketchnla import lowrank as _ref  # noqa: PLC0415
-        except ImportError:
-            raise ValueError(
-                "low_rank_approx(strategy='leverage_sample') samples rows by leverage scores "
-                "(outside this package); use 'srht_compose' or pass r_op and s_op"
-            ) from None
-        return _ref.low_rank_approx(a, k, eps, seed=seed, strategy=strategy, t_r=t_r, r_op=r_op,
-                                    s_op=s_op, **kw)
+        # leverage-score row samplers are another sketch family (SURVEY §2, out
+        # of scope); the reference's own low_rank_approx with shim.install()
+        # runs that strategy with its sparse-embedding column sketch on the GPU
+        raise ValueError(
+            "low_rank_approx(strategy='leverage_sample') samples rows by leverage scores "
+            "(outside this package); use 'srht_compose', pass r_op and s_op, or call "
+            "sketchnla.lowrank.low_rank_approx after paper_1207_6365_b200.install()"
+        )
     a = as_matrix(a)
     n, n_cols = a.shape
     k = check_count(k, "k")

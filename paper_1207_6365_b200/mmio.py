@@ -69,12 +69,15 @@ def load_matrix_market_device(path, device=None, n_threads: int = 0):
         indices = torch.empty(max(count, 1), dtype=torch.int32, device=device)
         out = torch.empty(max(count, 1), dtype=torch.float64, device=device)
         nnz = torch.zeros(1, dtype=torch.int64, device=device)
+        bad = torch.zeros(1, dtype=torch.int32, device=device)
         wsb = ctypes.c_size_t()
         _lib.check(L.skt_coo_to_csr_workspace(count, n_rows, n_cols, ctypes.byref(wsb)))
         ws = torch.empty(max(wsb.value, 8), dtype=torch.uint8, device=device)
         _lib.check(L.skt_coo_to_csr(_ptr(r), _ptr(c), _ptr(v), count, n_rows, n_cols, _ptr(indptr), _ptr(indices),
-                                    _ptr(out), _ptr(nnz), _ptr(ws), wsb.value, stream))
+                                    _ptr(out), _ptr(nnz), _ptr(bad), _ptr(ws), wsb.value, stream))
         k = int(nnz.item())
+        if int(bad.item()) != 0:  # as_csr(coo, path) (io.py:103, _validation.py:39-40)
+            raise ValueError(f"{path} contains non-finite entries")
     return (n_rows, n_cols), indptr, indices[:k], out[:k]
 
 

@@ -146,6 +146,23 @@ def _host(t: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def dense_operand(a: torch.Tensor) -> torch.Tensor:
+    """A device matrix in the layout K3 reads: 2-D (1-D -> one column), f32 or
+    f64 (other dtypes -> f64, as_dense's upcast), unit column stride, and rows
+    that do not overlap (a broadcast view such as ``x[None].expand(n, d)`` has
+    row stride 0 and is materialised)."""
+    if a.dim() == 1:
+        a = a.reshape(-1, 1)
+    if a.dim() != 2:
+        raise ValueError(f"matrix must be 2-D, got shape {tuple(a.shape)}")
+    if a.dtype not in _TORCH_TO_SKT:
+        a = a.to(torch.float64)
+    n, d = a.shape
+    if d > 0 and (a.stride(1) != 1 or (n > 1 and a.stride(0) < d)):
+        a = a.contiguous()
+    return a
+
+
 class SketchOperator:
     """Duck-typed protocol of the reference (sketch.py:97-119)."""
 
@@ -381,25 +398,25 @@ class SparseEmbedding(SketchOperator):
         dev_a = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
         return _host(self._apply_dense_device(dev_a, out_t, check_finite)).numpy()
 
-    def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None, buckets=None):
+    def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None, buckets=None,
+                            flag=None):
         """K3 on a device tensor.  ``buckets=(b0, b1)`` computes only SA rows
         [b0, b1) (the multi-GPU pipeline reduces finished bucket ranges while
-        the next range is computed)."""
+        the next range is computed).  ``flag`` (a 1-element int32 device
+        tensor) receives the fused non-finite scan without a host sync -- the
+        caller checks it (once, after a batch of calls); otherwise
+        ``check_finite`` syncs and raises ValueError like as_dense
+        (_validation.py:25-26)."""
         if a.device != self.device:
             raise ValueError(f"input on {a.device}, operator on {self.device}")
-        if a.dim() == 1:
-            a = a.reshape(-1, 1)
-        if a.dim() != 2:
-            raise ValueError(f"matrix must be 2-D, got shape {tuple(a.shape)}")
-        if a.dtype not in _TORCH_TO_SKT:
-            a = a.to(torch.float64)
-        if a.shape[1] > 0 and a.stride(1) != 1:
-            a = a.contiguous()
+        a = dense_operand(a)
         n, d = a.shape
         lda = max(a.stride(0), d, 1) if n > 1 else max(d, 1)
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
-        flag = torch.empty(1, dtype=torch.int32, device=self.device) if check_finite else None
+        sync_check = check_finite and flag is None
+        if sync_check:
+            flag = torch.empty(1, dtype=torch.int32, device=self.device)
         b0, b1 = (0, self.output_dim) if buckets is None else (int(buckets[0]), int(buckets[1]))
         if not (0 <= b0 < b1 <= self.output_dim):
             raise ValueError(f"bad bucket range {buckets!r}")
@@ -412,7 +429,7 @@ class SparseEmbedding(SketchOperator):
                     _stream_ptr(self.device),
                 )
             )
-        if check_finite and d > 0 and int(flag.item()) != 0:
+        if sync_check and d > 0 and int(flag.item()) != 0:
             raise ValueError("matrix contains non-finite entries")
         return out
 
@@ -590,17 +607,29 @@ def to_descriptor(s) -> dict:
 
 
 def from_descriptor(d: dict):
-    """sketch.py:460-465 for the families this package owns; other families
-    are handed to the reference package when it is importable."""
+    """sketch.py:460-478 for every family this package owns: the sparse
+    embedding, the generalized embedding and the SRHT come back as this
+    package's GPU classes.  The leverage sampler and Gaussian JL are other
+    sketch families outside the hot path; they raise instead of
+    silently running the reference's CPU code."""
     family = d.get("family")
     if family == "identity":
         return IdentityOperator(d["n"])
     if family == "sparse":
         return SparseEmbedding(d["n"], d["t"], d["seed"])
+    if family == "generalized":
+        from .generalized import GeneralizedSparseEmbedding  # noqa: PLC0415 (import cycle)
+
+        return GeneralizedSparseEmbedding(d["n"], d["r"], d["eps"], d["delta"], d["seed"])
+    if family == "srht":
+        from .solvers import SrhtOperator  # noqa: PLC0415 (import cycle)
+
+        return SrhtOperator(d["n"], d["t"], d["seed"], all_rows=d.get("all_rows", False))
     if family == "composed":
         return ComposedSketch(from_descriptor(d["outer"]), from_descriptor(d["inner"]))
-    try:
-        from sketchnla import sketch as _ref_sketch  # noqa: PLC0415
-    except ImportError:
-        raise ValueError(f"unknown sketch family {family!r}") from None
-    return _ref_sketch.from_descriptor(d)
+    if family in ("leverage", "gaussian"):
+        raise ValueError(
+            f"sketch family {family!r} is not provided by this package (outside the "
+            "CountSketch hot path); build it with sketchnla.sketch.from_descriptor"
+        )
+    raise ValueError(f"unknown sketch family {family!r}")

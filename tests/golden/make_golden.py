@@ -247,7 +247,7 @@ def mm_cases():
 
     from sketchnla.io import load_matrix_market
 
-    from tests.golden.mm_cases import BAD, GOOD
+    from tests.golden.mm_cases import BAD, GOOD, NONFINITE
 
     out, errors = {}, {}
     with tempfile.TemporaryDirectory() as tmp:
@@ -258,7 +258,7 @@ def mm_cases():
             m = load_matrix_market(p)
             out[f"{name}_indptr"], out[f"{name}_indices"], out[f"{name}_data"] = m.indptr, m.indices, m.data
             out[f"{name}_shape"] = np.asarray(m.shape)
-        for name, text in BAD.items():
+        for name, text in {**BAD, **NONFINITE}.items():
             p = os.path.join(tmp, f"{name}.mtx")
             with open(p, "w") as f:
                 f.write(text)
@@ -287,6 +287,9 @@ def seeds():
 
 if __name__ == "__main__":
     assert "reference" in os.path.dirname(sketchnla.__file__), sketchnla.__file__
+    if sys.argv[1:] == ["mm"]:  # regenerate only the Matrix Market fixtures
+        mm_cases()
+        sys.exit(0)
     seeds()
     srht_cases()
     gse_cases()

@@ -55,3 +55,12 @@ BAD = {
     "too_many": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 1.0\n2 2 2.0\n",
     "too_few": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n2 2 2.0\n",
 }
+
+# files that parse but whose canonical CSR holds a non-finite value: the
+# reference's as_csr(coo, path) raises ValueError("<path> contains non-finite
+# entries") (io.py:103, _validation.py:39-40)
+NONFINITE = {
+    "nonfinite_nan": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 2 nan\n",
+    "nonfinite_inf": "%%MatrixMarket matrix coordinate real general\n2 3 2\n1 3 -inf\n2 2 2.0\n",
+    "nonfinite_cancel": "%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n2 1 inf\n1 2 -inf\n3 3 1.0\n",
+}

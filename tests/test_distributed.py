@@ -46,10 +46,12 @@ def _worker(rank, world, port, n, t, d, seed, kind, q):
         else:
             a = sp.csr_array(sp.random_array((n, d), density=0.2, rng=rng, format="csr"))
 
-        def partial(a_local, out_dtype, buckets=None, out=None):
+        def partial(a_local, out_dtype, buckets=None, out=None, flag=None):
             r0, r1 = op.row_begin, op.row_end
             if isinstance(a_local, torch.Tensor):
                 a_local = a_local.numpy()
+            if flag is not None and kind == "dense" and not np.isfinite(a_local).all():
+                flag.fill_(1)  # the kernel's fused non-finite scan
             if kind == "dense":
                 p = O.apply_dense(h[r0:r1], s[r0:r1], t, a_local)
             else:
@@ -65,6 +67,12 @@ def _worker(rank, world, port, n, t, d, seed, kind, q):
             out_c = op.apply(torch.from_numpy(local), chunks=5).numpy()
             assert np.array_equal(out_c, out)
             assert op.bucket_chunks(5)[0][0] == 0 and op.bucket_chunks(5)[-1][1] == t
+            # a NaN on rank 1 only: both ranks raise (as_dense, _validation.py:25-26)
+            bad = torch.from_numpy(local.copy())
+            if rank == 1:
+                bad[7, 2] = float("nan")
+            with pytest.raises(ValueError, match="non-finite"):
+                op.apply(bad, chunks=3)
         if rank == 0:
             rel = np.linalg.norm(out - full) / max(np.linalg.norm(full), 1e-300)
             q.put((rel, op.row_begin, op.row_end))
@@ -142,3 +150,70 @@ def test_two_rank_gloo_bucket_ownership_matches_reference():
     same, b0, b1, rows = q.get(timeout=10)
     assert (b0, b1, rows) == (0, 50, 50)
     assert same
+
+
+# ---------------------------------------------------------------------------
+# The same two-rank layouts with the REAL kernels: both gloo ranks run their
+# shard operator (K1 with a row range, K2, K3/K4) on cuda:0; the collectives
+# move the partials through gloo (CPU), so no rank ever waits on another's
+# kernel.  This runs the sharded rejection offsets and bucket ranges
+# multi-process on the B200.
+# ---------------------------------------------------------------------------
+def _gpu_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import scipy.sparse as sp
+
+        from oracle import oracle as O
+        from paper_1207_6365_b200.distributed import BucketShardedSparseEmbedding
+
+        torch.cuda.set_device(0)
+        res = {}
+        # row shards, t with Lemire rejections (threshold 2^32 mod t != 0)
+        n, t, d, seed = 60_001, 25_000, 20, 11
+        rng = np.random.default_rng(9)
+        a = rng.standard_normal((n, d))
+        h, s = O.hash_signs(n, t, seed)
+        op = ShardedSparseEmbedding(n, t, seed, device="cuda:0")
+        r0, r1 = op.row_begin, op.row_end
+        res["h_shard"] = bool(np.array_equal(op.local.bucket, h[r0:r1].astype(np.int64)))
+        local = torch.from_numpy(a[r0:r1]).cuda()
+        part = op.partial_fn(local, torch.float64)
+        full = part.cpu()
+        dist.all_reduce(full)
+        ref = O.apply_dense(h, s, t, a)
+        res["rel_dense"] = float(np.linalg.norm(full.numpy() - ref) / np.linalg.norm(ref))
+        mine = O.apply_dense(h[r0:r1], s[r0:r1], t, a[r0:r1])
+        res["partial_exact"] = bool(np.array_equal(part.cpu().numpy(), mine))
+        # bucket ownership over CSR (config 5's layout), duplicate columns included
+        c = sp.csr_array(sp.random_array((n, 300), density=0.02, rng=rng, format="csr"))
+        cd = sp.csr_array((np.r_[c.data, 1.5], np.r_[c.indices, c.indices[c.indptr[4]]],
+                           np.r_[c.indptr[:5], c.indptr[5:] + 1]), shape=c.shape)  # row 4 repeats a column
+        bop = BucketShardedSparseEmbedding(n, t, seed, device="cuda:0")
+        tc = torch.sparse_csr_tensor(torch.from_numpy(cd.indptr).long(), torch.from_numpy(cd.indices).long(),
+                                     torch.from_numpy(cd.data), size=cd.shape)
+        blk = bop.apply(tc)
+        gathered = bop.gather(blk.cpu()).numpy()
+        res["bucket_exact"] = bool(np.array_equal(gathered, O.apply_csr(h, s, t, cd)))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gloo_real_kernels_on_gpu():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = q.get(timeout=10)
+    assert res["h_shard"] and res["partial_exact"] and res["bucket_exact"], res
+    assert res["rel_dense"] <= 1e-12, res

@@ -47,6 +47,31 @@ def test_unknown_family_rejected():
         S.from_descriptor({"family": "nope"})
 
 
+def test_no_reference_cpu_code_behind_the_package(monkeypatch):
+    """The families this package does not own raise instead of being handed to
+    the reference's CPU classes, and so does the leverage_sample low-rank
+    strategy -- even when the reference package is importable."""
+    import sys
+    import types
+
+    from paper_1207_6365_b200.lowrank import low_rank_approx
+
+    trap = types.ModuleType("sketchnla")
+    trap.__path__ = []  # any submodule import would fail loudly below
+
+    def _boom(*a, **k):  # pragma: no cover - must not be reached
+        raise AssertionError("product code reached the reference package")
+
+    trap.__getattr__ = _boom
+    monkeypatch.setitem(sys.modules, "sketchnla", trap)
+    for d in ({"family": "leverage", "probs": [0.5, 0.5], "t": 2, "seed": 0},
+              {"family": "gaussian", "rows": 2, "cols": 3, "seed": 0}):
+        with pytest.raises(ValueError, match="not provided by this package"):
+            S.from_descriptor(d)
+    with pytest.raises(ValueError, match="leverage_sample"):
+        low_rank_approx(np.ones((8, 6)), 2, 0.5, strategy="leverage_sample")
+
+
 def test_compose_dimension_check():
     with pytest.raises(ValueError):
         S.compose(S.IdentityOperator(4), S.IdentityOperator(5))

@@ -10,7 +10,7 @@ import pytest
 import scipy.sparse as sp
 
 from .conftest import GOLDEN
-from .golden.mm_cases import BAD, GOOD
+from .golden.mm_cases import BAD, GOOD, NONFINITE
 
 
 def _write(tmp_path, name, text):
@@ -117,3 +117,29 @@ def test_gpu_ingest_large_and_sketch(tmp_path):
     sa_dev = op.apply(as_torch_csr(shape, ip, ix, vv))
     sa_ref = op.apply(sp.csr_array((vv.cpu().numpy(), ix.cpu().numpy(), ip.cpu().numpy()), shape=shape))
     assert np.array_equal(sa_dev.cpu().numpy(), sa_ref)
+
+
+@pytest.mark.parametrize("name", sorted(NONFINITE))
+def test_nonfinite_files_parse_on_host(tmp_path, name):
+    """NaN / inf values are valid tokens for the parser (the reference's
+    float()); the rejection comes from the canonicalisation (next test)."""
+    from paper_1207_6365_b200.mmio import read_coo
+
+    shape, r, c, v = read_coo(_write(tmp_path, name, NONFINITE[name]))
+    assert not np.all(np.isfinite(v.numpy()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(NONFINITE))
+def test_gpu_nonfinite_rejected_like_reference(tmp_path, name):
+    """as_csr's finiteness check (io.py:103, _validation.py:39-40): the same
+    ValueError text as the reference, also when inf and -inf duplicates sum
+    to NaN (nonfinite_cancel)."""
+    from paper_1207_6365_b200.mmio import MatrixMarketError, load_matrix_market
+
+    want = json.load(open(os.path.join(GOLDEN, "mm_errors.json")))[name]
+    p = _write(tmp_path, name, NONFINITE[name])
+    with pytest.raises(ValueError) as e:
+        load_matrix_market(p)
+    assert not isinstance(e.value, MatrixMarketError)
+    assert str(e.value) == want.replace("{path}", p)
