@@ -58,6 +58,11 @@ def lib():
         L.oracle_apply_dense.argtypes = [P, P, P, i64, P, i32, i64, i64, P]
         L.oracle_apply_csr.argtypes = [P, P, i64, i64, P, P, P, i32, i64, P]
         L.oracle_lev_rownorms_csr.argtypes = [i64, P, P, P, i32, P, i64, P]
+        L.oracle_apply_dense_mt.argtypes = [P, P, P, i64, P, i32, i64, i64, P, i32]
+        L.oracle_apply_csr_mt.argtypes = [P, P, P, i64, P, P, P, i32, i64, P, i32]
+        L.oracle_lev_rownorms_csr_mt.argtypes = [i64, P, P, P, i32, P, i64, P, i32]
+        for f in ("oracle_apply_dense_mt", "oracle_apply_csr_mt", "oracle_lev_rownorms_csr_mt"):
+            getattr(L, f).restype = i32
         for f in ("oracle_seedseq_generate", "oracle_pcg64_seed", "oracle_hash_signs"):
             getattr(L, f).restype = i32
         _lib = L
@@ -127,7 +132,19 @@ def plan(h: np.ndarray, t: int):
     return indptr, rows
 
 
-def apply_dense(h, s, t: int, a: np.ndarray) -> np.ndarray:
+def _threads(threads: int) -> int:
+    """0 = every core this process may run on."""
+    if threads and threads > 0:
+        return int(threads)
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def apply_dense(h, s, t: int, a: np.ndarray, threads: int = 1) -> np.ndarray:
+    """Dense branch; ``threads != 1`` splits the buckets over host threads
+    (bit-identical: each SA element is summed by one thread in row order)."""
     a = np.asarray(a)
     if a.ndim == 1:
         a = a.reshape(-1, 1)
@@ -138,26 +155,48 @@ def apply_dense(h, s, t: int, a: np.ndarray) -> np.ndarray:
     d = a.shape[1]
     out = np.zeros((t, d), dtype=np.float64)
     s = np.ascontiguousarray(s, dtype=np.int8)
-    lib().oracle_apply_dense(
-        _ptr(indptr), _ptr(rows), _ptr(s), t, _ptr(a), int(a.dtype == np.float32), d, d, _ptr(out)
-    )
+    if threads == 1:
+        lib().oracle_apply_dense(
+            _ptr(indptr), _ptr(rows), _ptr(s), t, _ptr(a), int(a.dtype == np.float32), d, d, _ptr(out)
+        )
+    else:
+        rc = lib().oracle_apply_dense_mt(
+            _ptr(indptr), _ptr(rows), _ptr(s), t, _ptr(a), int(a.dtype == np.float32), d, d, _ptr(out),
+            _threads(threads),
+        )
+        assert rc == 0, "pthread_create failed"
     return out
 
 
-def apply_csr(h, s, t: int, a) -> np.ndarray:
+def _csr_parts(a):
     a = sp.csr_array(a)
     if a.data.dtype not in (np.float32, np.float64):
         a = sp.csr_array(a, dtype=np.float64)
-    n, d = a.shape
     indptr = np.ascontiguousarray(a.indptr, dtype=np.int64)
     indices = np.ascontiguousarray(a.indices, dtype=np.int32)
     vals = np.ascontiguousarray(a.data)
+    return a.shape, indptr, indices, vals
+
+
+def apply_csr(h, s, t: int, a, threads: int = 1) -> np.ndarray:
+    """CSR branch; ``threads != 1`` walks each bucket's rows (the plan) on
+    its own thread -- per element the same order as the nnz-order bincount."""
+    (n, d), indptr, indices, vals = _csr_parts(a)
     out = np.zeros((t, d), dtype=np.float64)
-    lib().oracle_apply_csr(
-        _ptr(np.ascontiguousarray(h, dtype=np.uint32)),
-        _ptr(np.ascontiguousarray(s, dtype=np.int8)),
-        n, t, _ptr(indptr), _ptr(indices), _ptr(vals), int(vals.dtype == np.float32), d, _ptr(out),
-    )
+    hh = np.ascontiguousarray(h, dtype=np.uint32)
+    ss = np.ascontiguousarray(s, dtype=np.int8)
+    if threads == 1:
+        lib().oracle_apply_csr(
+            _ptr(hh), _ptr(ss), n, t, _ptr(indptr), _ptr(indices), _ptr(vals), int(vals.dtype == np.float32), d,
+            _ptr(out),
+        )
+    else:
+        pptr, prow = plan(hh, t)
+        rc = lib().oracle_apply_csr_mt(
+            _ptr(pptr), _ptr(prow), _ptr(ss), t, _ptr(indptr), _ptr(indices), _ptr(vals),
+            int(vals.dtype == np.float32), d, _ptr(out), _threads(threads),
+        )
+        assert rc == 0, "pthread_create failed"
     return out
 
 
@@ -168,21 +207,16 @@ def apply(h, s, t: int, a) -> np.ndarray:
     return apply_dense(h, s, t, a)
 
 
-def lev_rownorms_csr(a, p: np.ndarray) -> np.ndarray:
-    a = sp.csr_array(a)
-    n, d = a.shape
+def lev_rownorms_csr(a, p: np.ndarray, threads: int = 1) -> np.ndarray:
+    (n, d), indptr, indices, vals = _csr_parts(a)
     p = np.ascontiguousarray(p, dtype=np.float64)
     out = np.zeros(n, dtype=np.float64)
-    lib().oracle_lev_rownorms_csr(
-        n,
-        _ptr(np.ascontiguousarray(a.indptr, dtype=np.int64)),
-        _ptr(np.ascontiguousarray(a.indices, dtype=np.int32)),
-        _ptr(np.ascontiguousarray(a.data)),
-        int(a.data.dtype == np.float32),
-        _ptr(p),
-        p.shape[1],
-        _ptr(out),
-    )
+    args = (n, _ptr(indptr), _ptr(indices), _ptr(vals), int(vals.dtype == np.float32), _ptr(p), p.shape[1],
+            _ptr(out))
+    if threads == 1:
+        lib().oracle_lev_rownorms_csr(*args)
+    else:
+        assert lib().oracle_lev_rownorms_csr_mt(*args, _threads(threads)) == 0, "pthread_create failed"
     return out
 
 

@@ -33,6 +33,7 @@
  * importable) and tests/test_oracle.py.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -259,4 +260,121 @@ void oracle_lev_rownorms_csr(int64_t n, const int64_t *indptr, const int32_t *in
     scores[i] = acc;
   }
   free(row);
+}
+
+/* ---------------- thread-parallel forms (same arithmetic) ----------------
+ * Full-size parity (configs 3-5) and the reference arm run these on all host
+ * cores.  Each output element keeps exactly the sequential order of the
+ * functions above -- buckets (dense, CSR) or rows (contraction) are split
+ * across threads, never the sum of one element -- so the results are
+ * bit-identical to the scalar restatement. */
+typedef struct {
+  int64_t lo, hi;             /* bucket / row range of this thread */
+  const int64_t *indptr;      /* plan (S in CSR) or CSR A */
+  const int32_t *rows;        /* plan rows */
+  const int8_t *s;
+  const void *a;              /* dense A, or CSR values */
+  const int64_t *a_indptr;    /* CSR A */
+  const int32_t *a_indices;
+  int is_f32;
+  int64_t d, lda;
+  const double *p;            /* contraction probe */
+  int64_t k;
+  double *out;
+} mt_job;
+
+static void *dense_worker(void *arg) {
+  mt_job *j = (mt_job *)arg;
+  int64_t cnt = j->hi - j->lo;
+  if (cnt > 0) {
+    /* buckets [lo, hi) of SA; the plan slice is rebased by pointer offset */
+    oracle_apply_dense(j->indptr + j->lo, j->rows, j->s, cnt, j->a, j->is_f32, j->d, j->lda,
+                       j->out + j->lo * j->d);
+  }
+  return NULL;
+}
+
+/* CSR branch by bucket: for bucket b, rows of b ascending (the plan), each
+ * row's entries in stored order -- per output element the same sequence as
+ * the nnz-order bincount of oracle_apply_csr. */
+static void *csr_worker(void *arg) {
+  mt_job *j = (mt_job *)arg;
+  for (int64_t b = j->lo; b < j->hi; ++b) {
+    double *y = j->out + b * j->d;
+    for (int64_t c = 0; c < j->d; ++c) y[c] = 0.0;
+    for (int64_t q = j->indptr[b]; q < j->indptr[b + 1]; ++q) {
+      int64_t i = j->rows[q];
+      double sg = (double)j->s[i];
+      for (int64_t e = j->a_indptr[i]; e < j->a_indptr[i + 1]; ++e) {
+        double v = j->is_f32 ? (double)((const float *)j->a)[e] : ((const double *)j->a)[e];
+        y[j->a_indices[e]] += sg * v;
+      }
+    }
+  }
+  return NULL;
+}
+
+static void *lev_worker(void *arg) {
+  mt_job *j = (mt_job *)arg;
+  int64_t cnt = j->hi - j->lo;
+  if (cnt > 0) {
+    /* rows [lo, hi): indptr is absolute, so shift the row pointer only */
+    oracle_lev_rownorms_csr(cnt, j->a_indptr + j->lo, j->a_indices, j->a, j->is_f32, j->p, j->k,
+                            j->out + j->lo);
+  }
+  return NULL;
+}
+
+static int run_jobs(void *(*fn)(void *), mt_job *proto, int64_t units, int nthreads, const int64_t *weight) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (units < nthreads) nthreads = units > 0 ? (int)units : 1;
+  pthread_t th[256];
+  mt_job jobs[256];
+  /* split by cumulative weight (rows per bucket / nnz per row) when given */
+  int64_t total = weight ? weight[units] - weight[0] : units;
+  int64_t lo = 0;
+  for (int w = 0; w < nthreads; ++w) {
+    int64_t hi;
+    if (w == nthreads - 1) {
+      hi = units;
+    } else if (weight) {
+      int64_t target = weight[0] + total * (w + 1) / nthreads;
+      hi = lo;
+      while (hi < units && weight[hi] < target) ++hi;
+    } else {
+      hi = units * (w + 1) / nthreads;
+    }
+    jobs[w] = *proto;
+    jobs[w].lo = lo;
+    jobs[w].hi = hi;
+    lo = hi;
+  }
+  for (int w = 0; w < nthreads; ++w)
+    if (pthread_create(&th[w], NULL, fn, &jobs[w]) != 0) return -1;
+  for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
+  return 0;
+}
+
+int oracle_apply_dense_mt(const int64_t *indptr, const int32_t *rows, const int8_t *s, int64_t t,
+                          const void *a, int is_f32, int64_t d, int64_t lda, double *sa, int nthreads) {
+  mt_job j = {0};
+  j.indptr = indptr; j.rows = rows; j.s = s; j.a = a; j.is_f32 = is_f32; j.d = d; j.lda = lda; j.out = sa;
+  return run_jobs(dense_worker, &j, t, nthreads, indptr);
+}
+
+int oracle_apply_csr_mt(const int64_t *plan_indptr, const int32_t *plan_rows, const int8_t *s, int64_t t,
+                        const int64_t *indptr, const int32_t *indices, const void *vals, int is_f32,
+                        int64_t d, double *sa, int nthreads) {
+  mt_job j = {0};
+  j.indptr = plan_indptr; j.rows = plan_rows; j.s = s; j.a = vals; j.a_indptr = indptr;
+  j.a_indices = indices; j.is_f32 = is_f32; j.d = d; j.out = sa;
+  return run_jobs(csr_worker, &j, t, nthreads, plan_indptr);
+}
+
+int oracle_lev_rownorms_csr_mt(int64_t n, const int64_t *indptr, const int32_t *indices, const void *vals,
+                               int is_f32, const double *p, int64_t k, double *scores, int nthreads) {
+  mt_job j = {0};
+  j.a_indptr = indptr; j.a_indices = indices; j.a = vals; j.is_f32 = is_f32; j.p = p; j.k = k; j.out = scores;
+  return run_jobs(lev_worker, &j, n, nthreads, indptr);
 }

@@ -108,3 +108,20 @@ def test_lev_contraction():
     rel = np.abs(got - z["scores"]) / np.maximum(np.abs(z["scores"]), 1e-300)
     assert rel.max() <= 1e-12
     assert np.allclose(O.np_lev_rownorms(a, z["probe"]), z["scores"], rtol=1e-13, atol=0)
+
+
+def test_threaded_oracle_equals_scalar_oracle():
+    """The thread-parallel forms used for full-size parity (configs 3-5) split
+    buckets / rows across threads, never one element's sum: bit-identical to
+    the scalar restatement, including t = 1 and t > n."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(1)
+    for n, t, d in [(100_000, 4_000, 20), (50_000, 1, 7), (3_000, 5_000, 3)]:
+        h, s = O.hash_signs(n, t, 5)
+        a = rng.standard_normal((n, d)).astype(np.float32)
+        assert np.array_equal(O.apply_dense(h, s, t, a), O.apply_dense(h, s, t, a, threads=0))
+        c = sp.csr_array(sp.random_array((n, d), density=0.3, rng=rng, format="csr"))
+        assert np.array_equal(O.apply_csr(h, s, t, c), O.apply_csr(h, s, t, c, threads=5))
+        p = rng.standard_normal((d, 8))
+        assert np.array_equal(O.lev_rownorms_csr(c, p), O.lev_rownorms_csr(c, p, threads=3))
