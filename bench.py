@@ -245,51 +245,75 @@ def gen_csr_shard(torch, cfg, r0, r1, device):
 # ---------------------------------------------------------------- arms
 def reference_arm(args, cfg):
     """The reference's CPU implementation of the path on this host: the oracle
-    port with the reference's own primitives (scipy CSR @ dense after the fp64
-    upcast + finiteness scan; repeat + bincount for CSR), single-threaded by
-    construction.  Each step = one bounded sample of the workload."""
+    port of sketch.py:153-165 with the reference's own primitives (dense:
+    as_dense's fp64 upcast + finiteness scan, then scipy's CSR @ dense =
+    csr_matvecs; CSR: repeat + bincount), single-threaded like the reference
+    (numpy / scipy C loops).  The input is the SAME matrix our arm times
+    (bench.py's seeded generators, generated on cuda:0 and copied to the host).
+    Configs 1, 2, 4, 5: each step is the whole apply.  Config 3 (about 34 s per
+    whole apply on one core): each step applies S to one 2^20-row block of the
+    full 16.7 M-row matrix, S's columns for those rows (the full operator's
+    buckets and signs, the same m x d output), cycling over the 16 blocks so
+    16 steps cover the whole workload once."""
     import numpy as np
-    import scipy.sparse as sp
+    import torch
 
     from oracle import oracle as O
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    sample_rows = {"c1": cfg["n"], "c2": cfg["n"], "c3": 1 << 18, "c4": 1 << 18}[args.config]
-    rng = np.random.default_rng(5)
-    h, s = O.hash_signs(sample_rows, cfg["m"], cfg["seed"])
-    mat = O.np_sketch_matrix(h, s, cfg["m"], sample_rows)
-    npdt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    n, d, m = cfg["n"], cfg["d"], cfg["m"]
+    gen_dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    t_prep = time.perf_counter()
+    h, s = O.hash_signs(n, m, cfg["seed"])
     if cfg["kind"] == "dense":
-        a = rng.standard_normal((sample_rows, cfg["d"])).astype(npdt)
-        if args.config == "c3":
-            a *= np.exp(rng.standard_normal((sample_rows, 1))).astype(npdt)
-        nnz = a.size
-        step = lambda: O.np_apply_dense(mat, a)  # noqa: E731
-    else:
-        from tests.synth import csr_fixed_nnz
+        blk = n if n <= (1 << 20) else (1 << 20)
+        a = np.empty((n, d), dtype=np.float32 if cfg["dtype"] == "f32" else np.float64)
+        for r0 in range(0, n, blk):
+            a[r0:r0 + blk] = gen_dense_shard(torch, cfg, r0, min(n, r0 + blk), gen_dev).cpu().numpy()
+        blocks = [(r0, min(n, r0 + blk)) for r0 in range(0, n, blk)]
+        mats = [O.np_sketch_matrix(h[r0:r1], s[r0:r1], m, r1 - r0) for r0, r1 in blocks]
+        nnz_per = [(r1 - r0) * d for r0, r1 in blocks]
 
-        a = csr_fixed_nnz(rng, sample_rows, cfg["d"], cfg["per_row"], dtype=npdt)
-        nnz = a.nnz
-        step = lambda: O.np_apply_csr(h, s, cfg["m"], a)  # noqa: E731
-    for _ in range(args.warmup):
-        step()
+        def step(j):
+            r0, r1 = blocks[j % len(blocks)]
+            O.np_apply_dense(mats[j % len(blocks)], a[r0:r1])
+            return nnz_per[j % len(blocks)]
+        sample = (f"whole apply of config 1" if len(blocks) == 1 else
+                  f"each step one {blk}-row block of the full {n}-row matrix with the full operator's "
+                  f"columns (same m x d output), cycling over the {len(blocks)} blocks")
+    else:
+        import scipy.sparse as sp
+
+        ip, ix, vv = gen_csr_shard(torch, cfg, 0, n, gen_dev)
+        a = sp.csr_array((vv.cpu().numpy(), ix.cpu().numpy(), ip.cpu().numpy()), shape=(n, d))
+        del ip, ix, vv
+
+        def step(j):
+            O.np_apply_csr(h, s, m, a)
+            return a.nnz
+        sample = "whole apply (the full matrix every step)"
+    prep_s = time.perf_counter() - t_prep
+    for j in range(args.warmup):
+        step(j)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
+    nnz = 0
+    for j in range(args.steps):
+        nnz += step(args.warmup + j)
     dt = time.perf_counter() - t0
-    value = nnz * args.steps / dt
+    value = nnz / dt
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "sample_rows": sample_rows, "d": cfg["d"], "m": cfg["m"]},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (the same seeded matrix as our arm)",
+        "config": {"workload": cfg["workload"], "n": n, "d": d, "m": m, "input_dtype": cfg["dtype"]},
         "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": "port",
-                         "sample": f"first {sample_rows} rows of the workload (same m, d, distribution); "
-                                   "reference primitives, single-threaded"},
+                         "sample": sample + "; reference primitives (sketch.py:153-165, _validation.py:16-27), "
+                                   "single-threaded like the reference", "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "prep_s": round(prep_s, 1),
     }
     return line
 
@@ -316,6 +340,28 @@ def cpu_baseline_sample(cfg_name, cfg, a_dev_sample, torch):
     return {"value": a.size / best, "unit": "nnz/s", "cores": 1, "kind": "port",
             "sample": f"rows [0, {rows}) of the workload x {cfg['d']} cols, best of {reps} "
                       "(scipy CSR @ dense after fp64 upcast, the reference's sketch.py:165 path)"}
+
+
+def cpu_baseline_csr(cfg, ip, ix, vv):
+    """Oracle port of sketch.py:155-164 (repeat + bincount) on the whole CSR
+    matrix of the workload, best of up to 5 within ~12 s, one core."""
+    import numpy as np
+    import scipy.sparse as sp
+
+    from oracle import oracle as O
+
+    n, d, m = cfg["n"], cfg["d"], cfg["m"]
+    a = sp.csr_array((vv.cpu().numpy(), ix.cpu().numpy(), ip.cpu().numpy()), shape=(n, d))
+    h, s = O.hash_signs(n, m, cfg["seed"])
+    best, reps, t_end = float("inf"), 0, time.perf_counter() + 12.0
+    while reps < 1 or (time.perf_counter() < t_end and reps < 5):
+        t0 = time.perf_counter()
+        O.np_apply_csr(h, s, m, a)
+        best = min(best, time.perf_counter() - t0)
+        reps += 1
+    return {"value": a.nnz / best, "unit": "nnz/s", "cores": 1, "kind": "port",
+            "sample": f"the whole matrix ({a.nnz} nnz), best of {reps} (repeat + bincount, "
+                      "the reference's sketch.py:155-164 path)"}
 
 
 def lowrank_report(args, cfg):
@@ -405,6 +451,8 @@ def our_arm(args, cfg):
 
     SA = torch.empty((m, d), dtype=sa_dt, device=dev)
     stream = torch.cuda.current_stream(dev)
+    fin_flags = torch.zeros((args.steps + args.warmup + 2) * max(1, args.chunks), dtype=torch.int32, device=dev)
+    fin_i = [0]
 
     lev = None
     if args.kernel == "lev":
@@ -427,7 +475,10 @@ def our_arm(args, cfg):
                 _TORCH_TO_SKT[vv.dtype], _ptr(lev[0]), lev[0].shape[1], _ptr(lev[1]), _lib.SKT_F64,
                 _stream_ptr(dev)))
         elif cfg["kind"] == "dense":
-            op._apply_dense_device(A, sa_dt, check_finite=False, out=SA)
+            # the API's work: the fused finiteness scan included (as_dense,
+            # _validation.py:25-26); the flag is read once after the timed loop
+            fin_i[0] += 1
+            op._apply_dense_device(A, sa_dt, out=SA, flag=fin_flags[fin_i[0] % fin_flags.numel()])
         else:
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
                                  deterministic=args.exact or not cfg.get("fast", False),
@@ -455,7 +506,9 @@ def our_arm(args, cfg):
         if pipelined:
             works = []
             for c0, c1 in ranges:
-                op._apply_dense_device(A, sa_dt, check_finite=False, out=SA, buckets=(c0, c1))
+                fin_i[0] += 1
+                op._apply_dense_device(A, sa_dt, out=SA, buckets=(c0, c1),
+                                       flag=fin_flags[fin_i[0] % fin_flags.numel()])
                 works.append(dist.all_reduce(SA[c0:c1], async_op=True))
             if kev is not None:
                 kev[1].record(stream)
@@ -505,6 +558,8 @@ def our_arm(args, cfg):
         return total_ms, kern_ms, launches, clk
 
     total_ms, kern_ms, launches, clk = timed_region()
+    if int(fin_flags.max()) != 0:
+        raise ValueError("matrix contains non-finite entries")
     remeasured = False
     if clk.rejected():
         log("clock check failed", clk.summary(), "- re-measuring once")
@@ -546,8 +601,8 @@ def our_arm(args, cfg):
                       "profiles/r01_gather_ceiling.json)"}
 
     # ---- end to end through the public API, host buffers
-    e2e = None
-    if not args.no_e2e and cfg["kind"] == "dense":
+    e2e, e2e_numpy = None, None
+    if not args.no_e2e and cfg["kind"] == "dense" and lev is None:
         host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
         host.copy_(A)
         torch.cuda.synchronize()
@@ -572,12 +627,48 @@ def our_arm(args, cfg):
                "d2h_bytes_per_step": res.numel() * res.element_size(),
                "steps": e_steps, "ms_per_step": 1e3 * float(e2e_s),
                "api": "SparseEmbedding.apply(pinned host tensor)"}
-        del host
+        if world == 1:
+            # the reference's calling convention: a pageable numpy ndarray in,
+            # a new fp64 numpy SA out (sketch.py:153-165)
+            arr = host.numpy()
+            del host
+            op.apply(arr)
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                res = op.apply(arr)
+            dt = (time.perf_counter() - t0) / e_steps
+            e2e_numpy = {"value": nnz_total / dt, "unit": "nnz/s", "h2d_bytes_per_step": arr.nbytes,
+                         "d2h_bytes_per_step": res.nbytes, "steps": e_steps, "ms_per_step": 1e3 * dt,
+                         "api": "SparseEmbedding.apply(numpy ndarray, pageable) -> numpy fp64"}
+            del arr
+        else:
+            del host
+    elif not args.no_e2e and cfg["kind"] == "csr" and lev is None and world == 1:
+        # scipy CSR in (the reference's convention; canonical, as as_csr leaves
+        # it), numpy fp64 SA out; every step copies indptr / indices / data
+        import scipy.sparse as sp
+
+        a_sp = sp.csr_array((vv.cpu().numpy(), ix.cpu().numpy(), ip.cpu().numpy()), shape=(n, d))
+        det = args.exact or not cfg.get("fast", False)
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        res = op.apply(a_sp, deterministic=det)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            res = op.apply(a_sp, deterministic=det)
+        dt = (time.perf_counter() - t0) / e_steps
+        e2e = {"value": nnz_total / dt, "unit": "nnz/s",
+               "h2d_bytes_per_step": a_sp.data.nbytes + a_sp.indices.nbytes + a_sp.indptr.nbytes,
+               "d2h_bytes_per_step": res.nbytes, "steps": e_steps, "ms_per_step": 1e3 * dt,
+               "api": "SparseEmbedding.apply(scipy.sparse.csr_array, pageable) -> numpy fp64"}
+        del a_sp
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg["kind"] == "dense":
-        rows = min(r1 - r0, 1 << 21)
-        cpu = cpu_baseline_sample(args.config, cfg, A[:rows], torch)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and lev is None:
+        if cfg["kind"] == "dense":
+            rows = min(r1 - r0, 1 << 21)
+            cpu = cpu_baseline_sample(args.config, cfg, A[:rows], torch)
+        else:
+            cpu = cpu_baseline_csr(cfg, ip, ix, vv)
 
     line = {
         "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps,
@@ -596,7 +687,7 @@ def our_arm(args, cfg):
                                   f"row-shard x{world}" + (
                        (f" + NCCL all-reduce of m x d partials, pipelined over {args.chunks} bucket ranges"
                         if pipelined else " + NCCL all-reduce of m x d partials") if world > 1 else "")},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_numpy": e2e_numpy, "gpu_launches": launches,
         "clocks": clk.summary(), "remeasured": remeasured,
         "build_ms": round(build_ms, 3), "kernel_ms_max_over_ranks": round(kern_ms_max, 4),
     }
@@ -622,7 +713,7 @@ def main():
                          "NVLink symmetric memory, owner slot sums, all-gather) instead of the NCCL all-reduce")
     ap.add_argument("--chunks", type=int, default=4,
                     help="N > 1: bucket ranges whose all-reduce overlaps the next range's compute")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
