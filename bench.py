@@ -42,9 +42,9 @@ CONFIGS = {
     "c4": dict(kind="csr", n=4_194_304, d=64, m=16_384, dtype="f32", per_row=16, dense_frac=0.01, seed=1,
                workload="config4: CSR fp32 4194304x64, 16 nnz/row + 1% dense rows N(0,100), m=16384"),
     "c5": dict(kind="csr", n=262_144, d=262_144, m=400, dtype="f32", per_row=262, lowrank=10, seed=1,
-               fast=True, shard="bucket",
+               shard="bucket",
                workload="config5: CSR fp32 262144x262144, 262 nnz/row (0.1%), values (U V^T)_ij + 0.01 N, "
-                        "rank 10; m=400 row sketch (fast mode: unordered fp32 atomics)"),
+                        "rank 10; m=400 row sketch"),
 }
 
 
@@ -143,10 +143,10 @@ def dominant_kernel(cfg, lev: bool, args, sa_dt) -> str:
         if 512 <= rb <= 2048 and rb % 16 == 0 and os.environ.get("SKT_DENSE_G4", "1") != "0":
             return "dense_g4_kernel (TMA tile::gather4 into an mbarrier smem ring)"
         return "apply_dense_kernel (register gather)"
-    if cfg.get("fast") and not args.exact:
+    if args.fast:
         return "csr_atomic_kernel (fast mode: unordered RED.ADD)"
-    if cfg["d"] > 256:
-        return "csr_rowseq_block_kernel (deterministic wide-d)"
+    if cfg["d"] > 25_000:
+        return "csr_colsweep_kernel (deterministic wide-d column sweep)"
     return "csr_group_kernel (grouped sweep)" if cfg.get("per_row", 16) <= 8 else "csr_tile_kernel (densify tiles)"
 
 
@@ -420,8 +420,7 @@ def our_arm(args, cfg):
     r0, r1 = (0, n) if bucket_mode else (rank * n // world, (rank + 1) * n // world)
     b0, b1 = (rank * m // world, (rank + 1) * m // world) if bucket_mode else (0, m)
     sa_dt = torch.float32 if cfg["dtype"] == "f32" else torch.float64
-    if args.exact and cfg.get("fast"):
-        sa_dt = torch.float64  # the deterministic wide-d kernel accumulates in the fp64 output row
+    fast = bool(args.fast)  # unordered atomics (not bit-exact); default: the deterministic kernels
 
     # ---- inputs resident in HBM
     if cfg["kind"] == "dense":
@@ -481,7 +480,7 @@ def our_arm(args, cfg):
             op._apply_dense_device(A, sa_dt, out=SA, flag=fin_flags[fin_i[0] % fin_flags.numel()])
         else:
             op._apply_csr_device(ip, ix, vv, d, sa_dt, canonical=True, out=SA,
-                                 deterministic=args.exact or not cfg.get("fast", False),
+                                 deterministic=not fast,
                                  buckets=(b0, b1) if bucket_mode else None)
 
     # N > 1, dense: pipelined exchange -- SA is computed in contiguous bucket
@@ -649,7 +648,7 @@ def our_arm(args, cfg):
         import scipy.sparse as sp
 
         a_sp = sp.csr_array((vv.cpu().numpy(), ix.cpu().numpy(), ip.cpu().numpy()), shape=(n, d))
-        det = args.exact or not cfg.get("fast", False)
+        det = not fast
         e_steps = max(1, min(args.steps, args.e2e_steps))
         res = op.apply(a_sp, deterministic=det)
         t0 = time.perf_counter()
@@ -706,8 +705,9 @@ def main():
     ap.add_argument("--kernel", default="sa", choices=["sa", "lev", "lowrank"],
                     help="sa: the S.A hot path (headline); lev: K5 leverage contraction (config c4); "
                          "lowrank: config 5 low-rank error ratio")
-    ap.add_argument("--exact", action="store_true",
-                    help="bit-exact deterministic kernels also for configs that default to fast mode (c5)")
+    ap.add_argument("--fast", action="store_true",
+                    help="CSR: unordered-atomics fast mode (equal to the reference up to rounding, not bit-exact)")
+    ap.add_argument("--exact", action="store_true", help="accepted for compatibility (exact is the default)")
     ap.add_argument("--fused", action="store_true",
                     help="dense, under torchrun: exchange fused into K3 (partial rows pushed to owner ranks over "
                          "NVLink symmetric memory, owner slot sums, all-gather) instead of the NCCL all-reduce")

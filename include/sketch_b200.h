@@ -129,6 +129,21 @@ skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, const uint
                          void *sa, skt_dtype sa_dtype, int64_t ldsa, uint32_t flags,
                          void *stream);
 
+/* skt_apply_csr_wide: K4 for CSR A whose SA rows are too wide for on-chip
+ * accumulators (BASELINE config 5: d = 262,144, t = 400) -- same contract and
+ * bit-identical result as skt_apply_csr (ascending row order per output from
+ * +0.0), for CANONICAL input (sorted, distinct column indices per row: as_csr
+ * output), shift-0 plan (indptr, rows).  One CTA per (bucket, column block)
+ * sweeps 8192-column super-steps with fp64 accumulators in shared memory and
+ * per-row cursors; no global atomics.  Workspace (device, caller-owned):
+ * skt_apply_csr_wide_workspace(n, t, d) bytes -- the per-row cursors. */
+skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, size_t *bytes);
+skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                              const void *a_indptr, skt_itype indptr_type, const void *a_indices,
+                              skt_itype index_type, const void *a_vals, skt_dtype val_dtype, int64_t nnz,
+                              int64_t d, void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws,
+                              size_t ws_bytes, void *stream);
+
 /* ---- column sketch A.S^T ------------------------------------------------ */
 /* Replaces apply_right (sketch.py:445-448) = (S.apply(A.T)).T without the
  * transpose: Y[i, h(j)] += s(j) A[i, j], per output ascending j.  A has

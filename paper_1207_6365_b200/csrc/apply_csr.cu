@@ -277,6 +277,7 @@ skt_status by_vals(const int64_t *pindptr, const uint32_t *prow, const uint8_t *
                        : launch<IP, IX, double, float>(pindptr, prow, blo, shift, t, n, aip, aix, av, nnz, d, sa, ldsa, flags, s);
 }
 
+
 }  // namespace
 }  // namespace skt
 
@@ -308,3 +309,4 @@ extern "C" skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows,
              ? by_vals<int64_t, int32_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s)
              : by_vals<int64_t, int64_t>(indptr, rows, blo, shift, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, flags, s);
 }
+

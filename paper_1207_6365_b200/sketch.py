@@ -443,16 +443,15 @@ class SparseEmbedding(SketchOperator):
         t x d ``out`` with those rows written."""
         if vals.dtype not in _TORCH_TO_SKT:
             vals = vals.to(torch.float64)
-        if (deterministic and out_dtype == torch.float32 and d > self._CSR_SMEM_MAX_D and canonical
-                and out is None):
-            # the wide deterministic kernel accumulates in the fp64 output row
-            return self._apply_csr_device(indptr, indices, vals, d, torch.float64, canonical,
-                                          buckets=buckets).to(torch.float32)
         if out is None:
             out = torch.empty((self.output_dim, d), dtype=out_dtype, device=self.device)
         b0, b1 = (0, self.output_dim) if buckets is None else (int(buckets[0]), int(buckets[1]))
         if not (0 <= b0 < b1 <= self.output_dim):
             raise ValueError(f"bad bucket range {buckets!r}")
+        if deterministic and canonical and d > self._CSR_SMEM_MAX_D:
+            # wide SA rows (config 5): the column-sweep kernel, shared-memory
+            # fp64 accumulators per 8192-column super-step, no global atomics
+            return self._apply_csr_wide(indptr, indices, vals, d, out, b0, b1)
         if shift is None:
             shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
         if b0 % (1 << shift):
@@ -467,6 +466,26 @@ class SparseEmbedding(SketchOperator):
                     _ITYPE[indices.dtype], _ptr(vals), _TORCH_TO_SKT[vals.dtype], vals.numel(), d,
                     _ptr(out) + b0 * out.stride(0) * out.element_size(), _TORCH_TO_SKT[out.dtype], max(d, 1),
                     flags, _stream_ptr(self.device),
+                )
+            )
+        return out
+
+    def _apply_csr_wide(self, indptr, indices, vals, d: int, out, b0: int, b1: int):
+        """skt_apply_csr_wide: rows [b0, b1) of SA for canonical CSR A with
+        wide rows (csrc/csr_colsweep.cuh); writes ``out`` directly in its dtype."""
+        L = _lib.lib()
+        m = self.row_end - self.row_begin
+        nb = ctypes.c_size_t()
+        check(L.skt_apply_csr_wide_workspace(m, b1 - b0, d, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            check(
+                L.skt_apply_csr_wide(
+                    _ptr(self.plan_indptr) + 8 * b0, _ptr(self.plan_rows), b1 - b0, m, _ptr(indptr),
+                    _ITYPE[indptr.dtype], _ptr(indices), _ITYPE[indices.dtype], _ptr(vals),
+                    _TORCH_TO_SKT[vals.dtype], vals.numel(), d,
+                    _ptr(out) + b0 * out.stride(0) * out.element_size(), _TORCH_TO_SKT[out.dtype],
+                    max(d, 1), _ptr(ws), nb.value, _stream_ptr(self.device),
                 )
             )
         return out
