@@ -211,7 +211,7 @@ skt_status skt_slot_sum(const void *recv, skt_dtype dtype, int32_t nslots, int64
 
 /* ---- passes of the preconditioned iterations and the rank-k residual ----- */
 /* SURVEY §8f rank 2, the passes over original data after the sketch.  M is
- * the n x r row-major fp64 product A R (regress.py:203, r <= 256); y, p are
+ * the n x r row-major fp64 product A R (regress.py:200, r <= 256); y, p are
  * r-vectors, b, q, rvec n-vectors (one right-hand-side column per call), all
  * fp64 on the device.  Reductions go through per-block partials in the
  * workspace (skt_lsq_workspace) and one fixed-order pass: deterministic.
@@ -224,7 +224,7 @@ skt_status skt_slot_sum(const void *recv, skt_dtype dtype, int32_t nslots, int64
  *    z = M^T rvec, *res2 = ||M y - b||^2 -- CGNR's r, z (regress.py:278-279)
  *    and the residual of the new iterate, one read of M.
  *  skt_spmm_csr: Y = A X (n x k, ldy), A CSR, X d x k fp64 -- M = A R for a
- *    sparse A (regress.py:203).
+ *    sparse A (regress.py:200).
  *  skt_gram_cross_csr / _dense: out2[0] = sum_i <A_i Mw, L_i>, out2[1] =
  *    ||A||_F^2 for Mw = W diag(d) (ncols x k, k <= 64) and L (n x k): the
  *    Gram-identity residual ||A - L D W^T||^2 = out2[1] - 2 out2[0] + sum d^2
@@ -240,6 +240,12 @@ skt_status skt_lsq_update_grad(int64_t n, int64_t r, const double *m, int64_t ld
                                int64_t ldq, double alpha, double *rvec, int64_t ldr, const double *y,
                                const double *b, int64_t ldb, double *z, double *res2, void *ws,
                                size_t ws_bytes, void *stream);
+/* skt_gemm_dense: Y = A X (n x k, ldy), A dense n x d (lda, f32 / f64), X
+ * d x k fp64 row-major, k <= 4096 -- M = A R for a dense A (regress.py:200),
+ * fp64 dot products in ascending column order (equal to numpy's BLAS product
+ * to rounding). */
+skt_status skt_gemm_dense(int64_t n, int64_t d, const void *a, skt_dtype a_dtype, int64_t lda, const double *x,
+                          int64_t k, double *y, int64_t ldy, void *stream);
 skt_status skt_spmm_csr(int64_t n, int64_t d, const void *a_indptr, skt_itype indptr_type,
                         const void *a_indices, skt_itype index_type, const void *a_vals,
                         skt_dtype val_dtype, int64_t nnz, const double *x, int64_t k, double *y,

@@ -53,6 +53,7 @@ EXPORTS = (
     "skt_lsq_residual_grad",
     "skt_lsq_matvec_norm",
     "skt_lsq_update_grad",
+    "skt_gemm_dense",
     "skt_spmm_csr",
     "skt_gram_cross_csr",
     "skt_gram_cross_dense",
@@ -151,6 +152,7 @@ def lib() -> ctypes.CDLL:
         "skt_lsq_residual_grad": ([i64, i64, P, i64, P, P, i64, P, P, P, sz, P], i32),
         "skt_lsq_matvec_norm": ([i64, i64, P, i64, P, P, i64, P, P, sz, P], i32),
         "skt_lsq_update_grad": ([i64, i64, P, i64, P, i64, ctypes.c_double, P, i64, P, P, i64, P, P, P, sz, P], i32),
+        "skt_gemm_dense": ([i64, i64, P, i32, i64, P, i64, P, i64, P], i32),
         "skt_spmm_csr": ([i64, i64, P, i32, P, i32, P, i32, i64, P, i64, P, i64, P], i32),
         "skt_gram_cross_csr": ([i64, i64, P, i32, P, i32, P, i32, P, i64, i64, P, i64, P, P, sz, P], i32),
         "skt_gram_cross_dense": ([i64, i64, P, i32, i64, P, i64, i64, P, i64, P, P, sz, P], i32),

@@ -217,6 +217,36 @@ __global__ void __launch_bounds__(kLsqThreads) spmm_csr_kernel(int64_t n, const 
   }
 }
 
+// ---- Y = A X for dense A (M = A R, regress.py:200) ---------------------------
+// One output element per thread (block = 256 consecutive elements of the
+// row-major n x k result); X is staged through shared memory in chunks of
+// rows, A[i, c] is read from L1/L2 (lanes of a warp share few rows); the dot
+// product runs over c in ascending order with fma, fp64.
+constexpr int kGemmChunk = 4096;  // doubles of X per shared-memory chunk (32 KB)
+
+template <typename TA>
+__global__ void __launch_bounds__(256) gemm_dense_kernel(int64_t n, int64_t d, const TA *__restrict__ a, int64_t lda,
+                                                         const double *__restrict__ x, int64_t k,
+                                                         double *__restrict__ y, int64_t ldy) {
+  __shared__ double xs[kGemmChunk];
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = e < n * k;
+  const int64_t i = live ? e / k : 0, j = live ? e - i * k : 0;
+  const int64_t rows = std::max<int64_t>(1, kGemmChunk / k);
+  double acc = 0.0;
+  for (int64_t c0 = 0; c0 < d; c0 += rows) {
+    const int64_t c1 = std::min<int64_t>(d, c0 + rows);
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < (c1 - c0) * k; q += blockDim.x) xs[q] = x[c0 * k + q];
+    __syncthreads();
+    if (live) {
+      const TA *ar = a + i * lda;
+      for (int64_t c = c0; c < c1; ++c) acc = fma((double)__ldg(ar + c), xs[(c - c0) * k + j], acc);
+    }
+  }
+  if (live) y[i * ldy + j] = acc;
+}
+
 // ---- Gram-identity residual: cross = sum_i <A_i M, L_i>, fro2 = sum a^2 ------
 // warp per row; lane takes stored entries p = rs + lane (+32): <M[col_p], L_i>
 // from L_i staged in shared memory (k <= 64)
@@ -488,5 +518,21 @@ extern "C" skt_status skt_gram_cross_dense(int64_t n, int64_t ncols, const void 
     SKT_LAUNCH(gram_dense_kernel<double>, (unsigned)blocks, kLsqThreads, 0, st, n, ncols, (const double *)a, lda, mw,
                ldm, (int)k, l, ldl, part);
   SKT_LAUNCH(lsq_final_kernel, 1, kLsqThreads, 0, st, part, (int)blocks, 2, out2);
+  return check_launch(fn);
+}
+
+extern "C" skt_status skt_gemm_dense(int64_t n, int64_t d, const void *a, skt_dtype a_dtype, int64_t lda,
+                                     const double *x, int64_t k, double *y, int64_t ldy, void *stream_) {
+  static const char *fn = "skt_gemm_dense";
+  if (n < 0 || d < 0 || k < 0 || k > kGemmChunk || lda < d || ldy < k || (a_dtype != SKT_F32 && a_dtype != SKT_F64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  if (n == 0 || k == 0) return SKT_OK;
+  if (!y || (d > 0 && (!a || !x))) return fail(SKT_EINVAL, fn, "NULL buffer");
+  cudaStream_t st = as_stream(stream_);
+  const int64_t blocks = (n * k + 255) / 256;
+  if (a_dtype == SKT_F32)
+    SKT_LAUNCH(gemm_dense_kernel<float>, (unsigned)blocks, 256, 0, st, n, d, (const float *)a, lda, x, k, y, ldy);
+  else
+    SKT_LAUNCH(gemm_dense_kernel<double>, (unsigned)blocks, 256, 0, st, n, d, (const double *)a, lda, x, k, y, ldy);
   return check_launch(fn);
 }

@@ -6,8 +6,8 @@ the reference's ``precondition``, ``richardson_solve`` and ``cgnr_solve``
   sketch (csrc/srht.cu) on the GPU -- both bit-identical to the reference --
   then the two pivoted QRs of the small sketches on the host with the
   reference's own LAPACK calls, so ``r_inv`` is identical.
-* ``_iterate``: M = A R formed on the device (cuBLAS GEMM for dense A, the
-  library's SpMM ``skt_spmm_csr`` for CSR), then each iteration is one or two
+* ``_iterate``: M = A R formed on the device by the library's own products
+  (``skt_gemm_dense`` for dense A, ``skt_spmm_csr`` for CSR), then each iteration is one or two
   fused passes over M (csrc/lsq.cu): Richardson needs one
   (``skt_lsq_residual_grad``: the residual of the current iterate that
   ``_iterate`` records and M^T (b - M y) for the next step, where the
@@ -106,7 +106,10 @@ class _Passes:
                                           _TORCH_TO_SKT[vv.dtype], vv.numel(), _ptr(r_dev), rank, _ptr(self.m),
                                           max(rank, 1), self.stream))
             else:
-                self.m = torch.from_numpy(np.ascontiguousarray(a)).to(device) @ r_dev  # plain GEMM (cuBLAS)
+                ad = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+                self.m = torch.empty((n, rank), dtype=torch.float64, device=device)
+                check(self.L.skt_gemm_dense(n, d, _ptr(ad), _TORCH_TO_SKT[ad.dtype], max(ad.stride(0), d, 1),
+                                            _ptr(r_dev), rank, _ptr(self.m), max(rank, 1), self.stream))
             self.m = self.m.contiguous()
         self.b = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(device)  # n x cols
         nb = ctypes.c_size_t()

@@ -155,3 +155,30 @@ def test_srht_operator_views_and_apply():
     assert full.output_dim == 128
     assert np.allclose(np.linalg.norm(full.apply(x)), np.linalg.norm(x), rtol=1e-13)
     assert srht_or_identity(50, 60, 1).family == "identity"
+
+
+@pytest.mark.parametrize("n,d,k,dtype,pad", [
+    (100_000, 20, 20, np.float64, 0),   # config 1's M = A R
+    (5_000, 300, 17, np.float32, 3),    # fp32 A, padded rows
+    (2_000, 5_000, 9, np.float64, 0),   # X staged in several shared-memory chunks
+    (7, 3, 1, np.float64, 1),
+])
+def test_gemm_dense_matches_numpy(n, d, k, dtype, pad):
+    """skt_gemm_dense (M = A R for a dense A, regress.py:200): fp64 dot products,
+    equal to numpy's BLAS product to rounding."""
+    import torch
+
+    from paper_1207_6365_b200 import _lib
+    from paper_1207_6365_b200.sketch import _TORCH_TO_SKT
+
+    rng = np.random.default_rng(n + d)
+    a = rng.standard_normal((n, d + pad)).astype(dtype)
+    x = rng.standard_normal((d, k))
+    ad = torch.from_numpy(a).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y = torch.empty((n, k), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().skt_gemm_dense(n, d, ad.data_ptr(), _TORCH_TO_SKT[ad.dtype], d + pad, xd.data_ptr(), k,
+                                         y.data_ptr(), k, torch.cuda.current_stream().cuda_stream))
+    ref = a[:, :d].astype(np.float64) @ x
+    err = np.abs(y.cpu().numpy() - ref).max() / max(np.abs(ref).max(), 1e-300)
+    assert err <= 1e-13, err
