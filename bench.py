@@ -136,6 +136,8 @@ def dominant_kernel(cfg, lev: bool, args, sa_dt) -> str:
     """Name of the kernel the line's roofline describes (the library picks it by
     shape)."""
     if lev:
+        if args.lev_f64:
+            return "lev_dmma_kernel (fp64 tensor cores, DMMA.8x8x4)"
         return "lev_tc3_kernel (tcgen05 kind::f16, scaled 2xFP16)"
     if cfg["kind"] == "dense":
         esz = 4 if cfg["dtype"] == "f32" else 8
@@ -429,6 +431,8 @@ def our_arm(args, cfg):
         in_bytes = A.numel() * A.element_size()
     else:
         ip, ix, vv = gen_csr_shard(torch, cfg, r0, r1, dev)
+        if args.kernel == "lev" and args.lev_f64:
+            vv = vv.double()  # as_csr's upcast: the dtype the reference API hands K5 (_validation.py:30-41)
         nnz_local = vv.numel()
         in_bytes = vv.numel() * (vv.element_size() + 4) + ip.numel() * ip.element_size()
     torch.cuda.synchronize()
@@ -705,6 +709,8 @@ def main():
     ap.add_argument("--kernel", default="sa", choices=["sa", "lev", "lowrank"],
                     help="sa: the S.A hot path (headline); lev: K5 leverage contraction (config c4); "
                          "lowrank: config 5 low-rank error ratio")
+    ap.add_argument("--lev-f64", action="store_true",
+                    help="--kernel lev: fp64 CSR values (the reference API's dtype) -> the fp64 tensor-core kernel")
     ap.add_argument("--fast", action="store_true",
                     help="CSR: unordered-atomics fast mode (equal to the reference up to rounding, not bit-exact)")
     ap.add_argument("--exact", action="store_true", help="accepted for compatibility (exact is the default)")

@@ -316,6 +316,12 @@ skt_status launch_dense(int64_t n, int64_t d, const void *a, int64_t lda, const 
 }  // namespace
 }  // namespace skt
 
+namespace skt {
+skt_status lev_dmma_csr(int64_t n, int64_t d, const void *aip, skt_itype ipt, const void *aix, skt_itype ixt,
+                        const void *av, skt_dtype vt, const double *p, int64_t k, void *scores, skt_dtype sdt,
+                        cudaStream_t st);
+}  // namespace skt
+
 using namespace skt;
 
 extern "C" skt_status skt_lev_rownorms_csr(int64_t n, int64_t d, const void *a_indptr,
@@ -332,6 +338,10 @@ extern "C" skt_status skt_lev_rownorms_csr(int64_t n, int64_t d, const void *a_i
   if (n == 0) return SKT_OK;
   if (!scores || (k > 0 && d > 0 && !probe)) return fail(SKT_EINVAL, fn, "NULL buffer");
   cudaStream_t st = as_stream(stream_);
+  // fp64 values (the reference API's dtype): the fp64 tensor-core kernel (lev_dmma.cuh)
+  const skt_status dm = lev_dmma_csr(n, d, a_indptr, indptr_type, a_indices, index_type, a_vals, val_dtype, probe, k,
+                                     scores, score_dtype, st);
+  if (dm != SKT_ENOTSUP) return dm;
   if (indptr_type == SKT_I32)
     return index_type == SKT_I32
                ? csr_types<int32_t, int32_t>(n, d, a_indptr, a_indices, a_vals, val_dtype, probe, k, scores, score_dtype, st)

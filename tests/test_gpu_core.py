@@ -620,3 +620,38 @@ def test_low_rank_approx_matches_reference():
     delta = float(np.sqrt(np.sum(sig[k:] ** 2)))
     assert abs(best_rank_k_error_gpu(a, k) - delta) <= 1e-6 * delta
     assert res.err >= delta * (1 - 1e-9)
+
+
+@pytest.mark.parametrize("n,d,k,density,itype", [
+    (20_000, 64, 32, 0.26, np.int32),   # config 4's shape
+    (3_001, 33, 16, 0.3, np.int64),     # d not a multiple of 4, int64 index arrays, partial last tile
+    (1_000, 20, 32, 1.0, np.int32),     # every row full (d <= 32 tile)
+    (2_500, 64, 32, 0.02, np.int32),    # many empty rows
+])
+def test_lev_fp64_tensor_core(n, d, k, density, itype, rng):
+    """fp64 CSR values (the reference API's dtype, as_csr's upcast) run on the
+    fp64 tensor cores (lev_dmma.cuh, DMMA.8x8x4): scores within 1e-12 relative
+    of the fp64 oracle (leverage.py:90-91), incl. rows scaled 1e-150 .. 1e150
+    and non-canonical rows (duplicates summed like scipy's a @ probe)."""
+    from paper_1207_6365_b200.solvers import lev_rownorms
+
+    a = sp.csr_array(sp.random_array((n, d), density=density, rng=rng, format="csr")).tolil()
+    a[5, :] = rng.standard_normal(d) * 1e150
+    a[9, :3] = 1e-150
+    a = sp.csr_array(a)
+    if n > 100:  # a duplicate column and an unsorted row
+        a = sp.csr_array((a.data.copy(), a.indices.copy(), a.indptr.copy()), shape=a.shape)
+        b, e = a.indptr[5], a.indptr[6]
+        a.indices[b + 1] = a.indices[b]
+        b, e = a.indptr[7], a.indptr[8]
+        a.indices[b:e] = a.indices[b:e][::-1].copy()
+    a = sp.csr_array((a.data, a.indices.astype(itype), a.indptr.astype(itype)), shape=a.shape)
+    probe = rng.standard_normal((d, k)) / np.sqrt(k)
+    ref = O.lev_rownorms_csr(a, probe)
+    got = lev_rownorms(a, probe)
+    nz = ref > 0
+    assert np.all(got[~nz] == 0)
+    assert np.max(np.abs(got[nz] - ref[nz]) / ref[nz]) <= 1e-12
+    got32 = lev_rownorms(a, probe, out_dtype=torch.float32)
+    fin = nz & (ref < 1e38) & (ref > 1e-37)  # scores representable in fp32
+    assert np.max(np.abs(got32[fin] - ref[fin]) / ref[fin]) <= 1e-6
