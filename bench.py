@@ -403,6 +403,7 @@ def lowrank_report(args, cfg):
 
 
 def our_arm(args, cfg):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -633,7 +634,7 @@ def our_arm(args, cfg):
         if world == 1:
             # the reference's calling convention: a pageable numpy ndarray in,
             # a new fp64 numpy SA out (sketch.py:153-165)
-            arr = host.numpy()
+            arr = np.array(host.numpy())  # a pageable copy (host is page-locked)
             del host
             op.apply(arr)
             t0 = time.perf_counter()

@@ -144,6 +144,14 @@ skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint6
                               int64_t d, void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* skt_memcpy_staged: copy between PAGEABLE host memory and the device through
+ * a ring of page-locked chunk buffers (host memcpy of chunk i + 1 overlaps the
+ * DMA of chunk i; the CUDA driver copies pageable memory at ~11 GB/s here,
+ * page-locked at ~55 GB/s).  kind 0 = host -> device: returns once src may be
+ * reused, the device data is ordered on `stream`; kind 1 = device -> host:
+ * returns when dst holds the data.  Serialised per device (one ring). */
+skt_status skt_memcpy_staged(void *dst, const void *src, size_t bytes, int32_t kind, void *stream);
+
 /* ---- column sketch A.S^T ------------------------------------------------ */
 /* Replaces apply_right (sketch.py:445-448) = (S.apply(A.T)).T without the
  * transpose: Y[i, h(j)] += s(j) A[i, j], per output ascending j.  A has
@@ -317,6 +325,13 @@ skt_status skt_mm_probe(const char *path, skt_mm_info *info);
 skt_status skt_mm_read_coo(const char *path, int64_t capacity, int64_t *rows, int64_t *cols, double *vals,
                            int64_t *count, int32_t n_threads);
 skt_status skt_coo_to_csr_workspace(int64_t count, int64_t n_rows, int64_t n_cols, size_t *bytes);
+/* skt_csr_check_sorted: *flag (device int32) = 1 if some row's column indices
+ * are not strictly increasing (duplicates / unsorted -- not as_csr's canonical
+ * form, _validation.py:30-41), else 0.  The device replacement for scipy's
+ * O(nnz) host scan (has_canonical_format) ahead of skt_apply_csr's
+ * SKT_CSR_CANONICAL flag. */
+skt_status skt_csr_check_sorted(int64_t n, const void *a_indptr, skt_itype indptr_type, const void *a_indices,
+                                skt_itype index_type, int32_t *flag, void *stream);
 skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, const double *vals, int64_t count,
                           int64_t n_rows, int64_t n_cols, int64_t *indptr, int32_t *indices, double *out_vals,
                           int64_t *nnz, int32_t *nonfinite, void *ws, size_t ws_bytes, void *stream);

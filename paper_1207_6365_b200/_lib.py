@@ -38,6 +38,8 @@ EXPORTS = (
     "skt_plan_build",
     "skt_apply_dense",
     "skt_apply_csr",
+    "skt_memcpy_staged",
+    "skt_csr_check_sorted",
     "skt_apply_csr_wide_workspace",
     "skt_apply_csr_wide",
     "skt_apply_dense_push",
@@ -137,6 +139,8 @@ def lib() -> ctypes.CDLL:
         "skt_plan_build": ([P, P, i64, u64, i32, P, P, P, P, sz, P], i32),
         "skt_apply_dense": ([P, P, u64, i64, P, i32, i64, i64, P, i32, i64, P, P], i32),
         "skt_apply_csr": ([P, P, P, i32, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, u32, P], i32),
+        "skt_memcpy_staged": ([P, P, sz, i32, P], i32),
+        "skt_csr_check_sorted": ([i64, P, i32, P, i32, P, P], i32),
         "skt_apply_csr_wide_workspace": ([i64, u64, i64, ctypes.POINTER(sz)], i32),
         "skt_apply_csr_wide": ([P, P, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, P, sz, P], i32),
         "skt_apply_dense_push": ([P, P, u64, i64, P, i32, i64, i64, i32, P, P, i32, i32, i64, i64, i64, P, P], i32),

@@ -169,3 +169,55 @@ extern "C" skt_status skt_coo_to_csr(const int64_t *rows, const int64_t *cols, c
   SKT_LAUNCH(coo_indptr_kernel, gridn(n_rows + 1), 256, 0, st, w.rowcnt, n_rows + 1, indptr, w.part + nbr, nnz);
   return check_launch(fn);
 }
+
+// ---- canonical-format check on the device --------------------------------
+// *flag = 1 if some row's column indices are not strictly increasing
+// (duplicates or unsorted: not as_csr's canonical form, _validation.py:30-41)
+// -- replaces scipy's O(nnz) host scan (has_canonical_format) before choosing
+// the S.A kernel.  The flag is zeroed first.  Warp per 32 entries: entry p is
+// checked against entry p - 1 unless p starts its row.
+template <typename IP, typename IX>
+__global__ void csr_sorted_kernel(int64_t n, const IP *__restrict__ aip, const IX *__restrict__ aix,
+                                  int32_t *__restrict__ flag) {
+  const int64_t nnz = (int64_t)aip[n];
+  const int64_t base = (int64_t)aip[0];
+  bool bad = false;
+  for (int64_t p = base + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (!(__ldg(aix + p) > __ldg(aix + p - 1))) {
+      // a row start between p - 1 and p makes the pair unrelated
+      int64_t lo = 0, hi = n;  // last row r with aip[r] <= p
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)aip[mid] <= p) lo = mid; else hi = mid;
+      }
+      if ((int64_t)aip[lo] != p) bad = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+extern "C" skt_status skt_csr_check_sorted(int64_t n, const void *a_indptr, skt_itype indptr_type,
+                                           const void *a_indices, skt_itype index_type, int32_t *flag,
+                                           void *stream_) {
+  static const char *fn = "skt_csr_check_sorted";
+  if (n < 0 || !a_indptr || !flag || (indptr_type != SKT_I32 && indptr_type != SKT_I64) ||
+      (index_type != SKT_I32 && index_type != SKT_I64))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  cudaStream_t st = as_stream(stream_);
+  SKT_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t), st), fn);
+  if (n == 0) return SKT_OK;
+  const unsigned blocks = (unsigned)kNumSMs * 8;
+  if (indptr_type == SKT_I32) {
+    if (index_type == SKT_I32)
+      SKT_LAUNCH((csr_sorted_kernel<int32_t, int32_t>), blocks, 256, 0, st, n, (const int32_t *)a_indptr, (const int32_t *)a_indices, flag);
+    else
+      SKT_LAUNCH((csr_sorted_kernel<int32_t, int64_t>), blocks, 256, 0, st, n, (const int32_t *)a_indptr, (const int64_t *)a_indices, flag);
+  } else {
+    if (index_type == SKT_I32)
+      SKT_LAUNCH((csr_sorted_kernel<int64_t, int32_t>), blocks, 256, 0, st, n, (const int64_t *)a_indptr, (const int32_t *)a_indices, flag);
+    else
+      SKT_LAUNCH((csr_sorted_kernel<int64_t, int64_t>), blocks, 256, 0, st, n, (const int64_t *)a_indptr, (const int64_t *)a_indices, flag);
+  }
+  return check_launch(fn);
+}

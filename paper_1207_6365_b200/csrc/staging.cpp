@@ -1,0 +1,178 @@
+// staging.cpp -- host <-> device copies of PAGEABLE host memory (numpy arrays,
+// the reference's calling convention: sketch.py:153-165 takes ndarray / scipy
+// CSR and returns a new ndarray).  The CUDA driver copies pageable memory at
+// ~11 GB/s on this platform against ~55 GB/s from page-locked memory
+// (tools/e2e_csr_probe.py), so skt_memcpy_staged pipelines the copy through a
+// ring of page-locked chunk buffers: host threads memcpy chunk i + 1 into a
+// free buffer while the DMA engine moves chunk i.  The ring (4 x 16 MB per
+// device) and the worker threads are created on first use and reused.
+//
+//   kind 0 (H2D): returns once the source may be reused (the last DMAs are
+//                 stream-ordered before later work on `stream`);
+//   kind 1 (D2H): returns when dst holds the data (waits for the stream).
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skt {
+namespace {
+
+constexpr size_t kChunk = 16u << 20;
+constexpr int kRing = 4;
+
+// fixed pool of memcpy workers: parallel_copy splits one memcpy into slices
+class CopyPool {
+ public:
+  CopyPool() {
+    unsigned hw = std::thread::hardware_concurrency();
+    nthreads_ = (int)std::max(1u, std::min(8u, hw > 1 ? hw / 2 : 1u));
+    for (int i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : workers_) t.join();
+  }
+  void copy(void *dst, const void *src, size_t bytes) {
+    if (bytes < (1u << 20) || nthreads_ == 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_m_);  // one parallel copy at a time
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = (char *)dst;
+      src_ = (const char *)src;
+      bytes_ = bytes;
+      pending_ = nthreads_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    slice(0);
+    std::unique_lock<std::mutex> g(m_);
+    done_cv_.wait(g, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void slice(int i) {
+    const size_t per = (bytes_ / nthreads_ + 63) & ~(size_t)63;
+    const size_t b = std::min(bytes_, per * i), e = std::min(bytes_, per * (i + 1));
+    if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
+  }
+  void run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      slice(i);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  int nthreads_ = 1;
+  std::vector<std::thread> workers_;
+  std::mutex m_, call_m_;
+  std::condition_variable cv_, done_cv_;
+  bool stop_ = false;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  char *dst_ = nullptr;
+  const char *src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+CopyPool &pool() {
+  static CopyPool p;
+  return p;
+}
+
+struct Ring {
+  void *buf[kRing] = {};
+  cudaEvent_t ev[kRing] = {};
+  std::mutex m;  // one staged copy per device at a time
+};
+
+skt_status ring_for_device(Ring **out) {
+  static std::mutex m;
+  static std::map<int, Ring *> rings;
+  int dev = 0;
+  SKT_CUDA_TRY(cudaGetDevice(&dev), "skt_memcpy_staged");
+  std::lock_guard<std::mutex> g(m);
+  Ring *&r = rings[dev];
+  if (!r) {
+    Ring *nr = new Ring;
+    for (int i = 0; i < kRing; ++i) {
+      if (cudaHostAlloc(&nr->buf[i], kChunk, cudaHostAllocPortable) != cudaSuccess ||
+          cudaEventCreateWithFlags(&nr->ev[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(SKT_ECUDA, "skt_memcpy_staged", "page-locked staging ring allocation failed");
+    }
+    r = nr;
+  }
+  *out = r;
+  return SKT_OK;
+}
+
+}  // namespace
+}  // namespace skt
+
+using namespace skt;
+
+extern "C" skt_status skt_memcpy_staged(void *dst, const void *src, size_t bytes, int32_t kind, void *stream_) {
+  static const char *fn = "skt_memcpy_staged";
+  if ((kind != 0 && kind != 1) || (bytes > 0 && (!dst || !src))) return fail(SKT_EINVAL, fn, "bad arguments");
+  if (bytes == 0) return SKT_OK;
+  cudaStream_t st = as_stream(stream_);
+  Ring *r = nullptr;
+  skt_status s = ring_for_device(&r);
+  if (s != SKT_OK) return s;
+  std::lock_guard<std::mutex> g(r->m);
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  if (kind == 0) {  // host (pageable) -> device
+    for (size_t i = 0; i < nch; ++i) {
+      const int b = (int)(i % kRing);
+      const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+      SKT_CUDA_TRY(cudaEventSynchronize(r->ev[b]), fn);  // the DMA that last read buffer b is done
+      pool().copy(r->buf[b], (const char *)src + off, len);
+      SKT_CUDA_TRY(cudaMemcpyAsync((char *)dst + off, r->buf[b], len, cudaMemcpyHostToDevice, st), fn);
+      SKT_CUDA_TRY(cudaEventRecord(r->ev[b], st), fn);
+    }
+    // the caller may reuse src now; the ring buffers stay owned by the DMAs
+    // until their events complete (checked before the next reuse)
+    return SKT_OK;
+  }
+  // device -> host (pageable): chunks DMA'd ahead into the ring, drained in order
+  size_t issued = 0;
+  auto issue = [&](size_t i) -> skt_status {
+    const int b = (int)(i % kRing);
+    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    SKT_CUDA_TRY(cudaMemcpyAsync(r->buf[b], (const char *)src + off, len, cudaMemcpyDeviceToHost, st), fn);
+    SKT_CUDA_TRY(cudaEventRecord(r->ev[b], st), fn);
+    return SKT_OK;
+  };
+  for (; issued < nch && issued < (size_t)kRing; ++issued)
+    if ((s = issue(issued)) != SKT_OK) return s;
+  for (size_t i = 0; i < nch; ++i) {
+    const int b = (int)(i % kRing);
+    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    SKT_CUDA_TRY(cudaEventSynchronize(r->ev[b]), fn);
+    pool().copy((char *)dst + off, r->buf[b], len);
+    if (issued < nch) {
+      if ((s = issue(issued)) != SKT_OK) return s;
+      ++issued;
+    }
+  }
+  return SKT_OK;
+}

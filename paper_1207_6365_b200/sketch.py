@@ -146,6 +146,31 @@ def _host(t: torch.Tensor) -> torch.Tensor:
     return out
 
 
+_STAGE_MIN = 4 << 20  # host arrays below this go through torch's own copy
+
+
+def _to_device(x: np.ndarray, device) -> torch.Tensor:
+    """numpy array (pageable host memory) -> new device tensor, through the
+    library's page-locked staging ring (skt_memcpy_staged) for large arrays."""
+    x = np.ascontiguousarray(x)
+    if x.nbytes < _STAGE_MIN:
+        return torch.from_numpy(x).to(device)
+    out = torch.empty(x.shape, dtype=torch.from_numpy(x[:0]).dtype, device=device)
+    with torch.cuda.device(device):
+        check(_lib.lib().skt_memcpy_staged(_ptr(out), x.ctypes.data, x.nbytes, 0, _stream_ptr(device)))
+    return out
+
+
+def csr_is_canonical_device(indptr: torch.Tensor, indices: torch.Tensor, n: int) -> bool:
+    """Strictly increasing column indices in every row (skt_csr_check_sorted);
+    one 4-byte device->host read."""
+    flag = torch.empty(1, dtype=torch.int32, device=indptr.device)
+    with torch.cuda.device(indptr.device):
+        check(_lib.lib().skt_csr_check_sorted(n, _ptr(indptr), _ITYPE[indptr.dtype], _ptr(indices),
+                                              _ITYPE[indices.dtype], _ptr(flag), _stream_ptr(indptr.device)))
+    return int(flag.item()) == 0
+
+
 def dense_operand(a: torch.Tensor) -> torch.Tensor:
     """A device matrix in the layout K3 reads: 2-D (1-D -> one column), f32 or
     f64 (other dtypes -> f64, as_dense's upcast), unit column stride, and rows
@@ -369,7 +394,8 @@ class SparseEmbedding(SketchOperator):
                 parts = (a.crow_indices(), a.col_indices(), a.values())
                 if not a.is_cuda:
                     parts = tuple(x.to(self.device, non_blocking=True) for x in parts)
-                res = self._apply_csr_device(*parts, a.shape[1], out_t, canonical=False,
+                res = self._apply_csr_device(*parts, a.shape[1], out_t,
+                                             canonical=csr_is_canonical_device(parts[0], parts[1], a.shape[0]),
                                              deterministic=deterministic)
                 return res if a.is_cuda else _host(res)
             if a.is_cuda:
@@ -378,14 +404,14 @@ class SparseEmbedding(SketchOperator):
             return _host(self._apply_dense_device(dev_a, out_t, check_finite))
         out_t = torch.float64 if out_dtype is None else out_dtype
         if sp.issparse(a):
-            m = sp.csr_array(a)
+            m = a if a.format == "csr" else sp.csr_array(a)
             if m.data.dtype not in (np.float32, np.float64):
                 m = sp.csr_array(m, dtype=np.float64)
-            canonical = bool(m.has_canonical_format)
             dev = self.device
-            ip = torch.from_numpy(np.ascontiguousarray(m.indptr)).to(dev)
-            ix = torch.from_numpy(np.ascontiguousarray(m.indices)).to(dev)
-            vv = torch.from_numpy(np.ascontiguousarray(m.data)).to(dev)
+            ip, ix, vv = (_to_device(x, dev) for x in (m.indptr, m.indices, m.data))
+            # canonical form checked on the device (scipy's has_canonical_format
+            # is an O(nnz) host scan on every new csr object)
+            canonical = csr_is_canonical_device(ip, ix, m.shape[0])
             return _host(self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical,
                                                 deterministic=deterministic)).numpy()
         arr = np.asarray(a)
@@ -395,7 +421,7 @@ class SparseEmbedding(SketchOperator):
             arr = arr.reshape(-1, 1)
         if arr.ndim != 2:
             raise ValueError(f"matrix must be 2-D, got shape {arr.shape}")
-        dev_a = torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
+        dev_a = _to_device(arr, self.device)
         return _host(self._apply_dense_device(dev_a, out_t, check_finite)).numpy()
 
     def _apply_dense_device(self, a: torch.Tensor, out_dtype, check_finite=True, out=None, buckets=None,

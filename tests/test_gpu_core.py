@@ -655,3 +655,42 @@ def test_lev_fp64_tensor_core(n, d, k, density, itype, rng):
     got32 = lev_rownorms(a, probe, out_dtype=torch.float32)
     fin = nz & (ref < 1e38) & (ref > 1e-37)  # scores representable in fp32
     assert np.max(np.abs(got32[fin] - ref[fin]) / ref[fin]) <= 1e-6
+
+
+def test_csr_check_sorted_device(rng):
+    """skt_csr_check_sorted: the device form of scipy's has_canonical_format
+    (strictly increasing columns per row), incl. empty rows, a duplicate at a
+    row start, and int64 index arrays."""
+    from paper_1207_6365_b200.sketch import csr_is_canonical_device
+
+    for it in (np.int32, np.int64):
+        a = sp.csr_array(sp.random_array((5_000, 300), density=0.05, rng=rng, format="csr"))
+        ip, ix = (torch.from_numpy(x.astype(it)).cuda() for x in (a.indptr, a.indices))
+        assert a.has_canonical_format and csr_is_canonical_device(ip, ix, a.shape[0])
+        for r in (0, 1234, 4999):  # duplicate / unsorted pair inside one row
+            b, e = a.indptr[r], a.indptr[r + 1]
+            if e - b < 2:
+                continue
+            bad = a.indices.copy()
+            bad[e - 1] = bad[e - 2]
+            ixb = torch.from_numpy(bad.astype(it)).cuda()
+            assert not csr_is_canonical_device(ip, ixb, a.shape[0])
+        # a smaller column at a row start is canonical (different rows)
+        z = sp.csr_array((np.ones(4), np.array([5, 7, 1, 2]), np.array([0, 2, 2, 4])), shape=(3, 9))
+        ipz, ixz = (torch.from_numpy(x.astype(it)).cuda() for x in (z.indptr, z.indices))
+        assert csr_is_canonical_device(ipz, ixz, 3)
+
+
+@pytest.mark.parametrize("nbytes", [1, 4_000_003, 16 << 20, (16 << 20) * 4 + 12345, (16 << 20) * 9 + 8])
+def test_memcpy_staged_round_trip(nbytes):
+    """skt_memcpy_staged (page-locked ring for pageable host memory): both
+    directions byte-exact for sizes below, at and across the 16 MB chunks and
+    the 4-buffer ring."""
+    host = np.frombuffer(np.random.default_rng(nbytes).bytes(nbytes), dtype=np.uint8).copy()
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(_lib.lib().skt_memcpy_staged(dev.data_ptr(), host.ctypes.data, nbytes, 0, st))
+    assert torch.equal(dev.cpu(), torch.from_numpy(host))
+    back = np.zeros(nbytes, dtype=np.uint8)
+    _lib.check(_lib.lib().skt_memcpy_staged(back.ctypes.data, dev.data_ptr(), nbytes, 1, st))
+    assert np.array_equal(back, host)
