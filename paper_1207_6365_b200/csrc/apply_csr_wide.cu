@@ -1,7 +1,10 @@
 // apply_csr_wide.cu -- K4 for CSR A too wide for on-chip accumulators of
 // whole SA rows: the column-sweep kernel (csr_colsweep.cuh) behind
 // skt_apply_csr_wide (sketch.py:155-164, BASELINE config 5).
+#include <cstdlib>
+
 #include "common.cuh"
+#include "csr_colblock.cuh"
 #include "csr_colsweep.cuh"
 
 namespace skt {
@@ -30,11 +33,42 @@ inline ColsweepGeom colsweep_geom(uint64_t t, int64_t d) {
   return ColsweepGeom{(int)nblk, per * kCsStep};
 }
 
+// SKT_CSR_WIDE=colsweep selects the column-sweep kernel (A/B)
+inline bool use_colsweep() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_CSR_WIDE");
+    return e && e[0] == 'c' && e[3] == 's';
+  }();
+  return on;
+}
+inline int colblock_nblk(int64_t d) { return (int)std::max<int64_t>(1, (d + kCbCols - 1) / kCbCols); }
+
+template <typename IP, typename IX, typename TV, typename TOut>
+skt_status launch_colblock(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
+                           const void *aix, const void *av, int64_t d, void *sa, int64_t ldsa, int32_t *bnd,
+                           cudaStream_t stream) {
+  static const char *fn = "skt_apply_csr_wide";
+  const int nblk = colblock_nblk(d);
+  if (nblk > 1 && n > 0) {
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * 16);
+    SKT_LAUNCH((csr_colblock_bounds_kernel<IP, IX>), (unsigned)blocks, 256, 0, stream, n, nblk, (const IP *)aip,
+               (const IX *)aix, bnd);
+    SKT_CUDA_TRY(cudaGetLastError(), fn);
+  }
+  auto k = csr_colblock_kernel<IP, IX, TV, TOut>;
+  const int smem = (int)sizeof(CbSmem);
+  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), fn);
+  SKT_LAUNCH(k, (unsigned)(t * nblk), kCbThreads, smem, stream, pindptr, prow, nblk, d, (const IP *)aip,
+             (const IX *)aix, (const TV *)av, bnd, (TOut *)sa, ldsa);
+  return check_launch(fn);
+}
+
 template <typename IP, typename IX, typename TV, typename TOut>
 skt_status launch_colsweep(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
                            const void *aix, const void *av, int64_t d, void *sa, int64_t ldsa, int32_t *cursor,
                            cudaStream_t stream) {
   static const char *fn = "skt_apply_csr_wide";
+  if (!use_colsweep()) return launch_colblock<IP, IX, TV, TOut>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, stream);
   const ColsweepGeom g = colsweep_geom(t, d);
   const int64_t items = (int64_t)n * g.nblk;
   if (items > 0) {
@@ -68,7 +102,9 @@ using namespace skt;
 
 extern "C" skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, size_t *bytes) {
   if (!bytes || n < 0 || t < 1 || d < 0) return fail(SKT_EINVAL, "skt_apply_csr_wide_workspace", "bad arguments");
-  *bytes = (size_t)std::max<int64_t>(1, n) * (size_t)colsweep_geom(t, d).nblk * sizeof(int32_t);
+  const size_t sweep = (size_t)std::max<int64_t>(1, n) * (size_t)colsweep_geom(t, d).nblk * sizeof(int32_t);
+  const size_t block = (size_t)std::max<int64_t>(1, n) * (size_t)std::max(1, colblock_nblk(d) - 1) * sizeof(int32_t);
+  *bytes = std::max(sweep, block);
   return SKT_OK;
 }
 

@@ -44,43 +44,43 @@ __host__ __device__ constexpr int tile_slice_bytes() {
 // row; row descriptors from shared memory (broadcast).
 template <int G, typename IX, typename TV>
 __device__ __forceinline__ void load_rows(const int4 *__restrict__ desc, int nrows, const IX *__restrict__ aix,
-                                          const TV *__restrict__ av, int lane, IX (&cc)[16], TV (&vv)[16]) {
+                                          const TV *__restrict__ av, int lane, int32_t (&cc)[16], TV (&vv)[16]) {
   constexpr int S = 32 / G;
   const int g = lane / G, gl = lane % G;
 #pragma unroll
   for (int i = 0; i < G; ++i) {
     const int r = i * S + g;
-    cc[i] = (IX)-1;
+    cc[i] = -1;  // columns < d <= 256: int32 registers for any index type
     if (i * S < nrows) {  // warp-uniform
       const int4 ds = desc[r];
       const int64_t rs = (int64_t)(uint32_t)ds.x | ((int64_t)ds.y << 32);
       if (r < nrows && gl < ds.z) {
-        cc[i] = __ldg(aix + rs + gl);
+        cc[i] = (int32_t)__ldg(aix + rs + gl);
         vv[i] = __ldg(av + rs + gl);
       }
     }
   }
 }
 
-template <int G, typename IX, typename TV>
+template <int G, typename TV>
 __device__ __forceinline__ void store_rows(const int4 *__restrict__ desc, TV *tile, int dp, int lane,
-                                           const IX (&cc)[16], const TV (&vv)[16]) {
+                                           const int32_t (&cc)[16], const TV (&vv)[16]) {
   constexpr int S = 32 / G;
   const int g = lane / G;
 #pragma unroll
   for (int i = 0; i < G; ++i) {
     const int r = i * S + g;
-    if (cc[i] != (IX)-1) tile[r * dp + (int)cc[i]] = desc[r].w ? -vv[i] : vv[i];
+    if (cc[i] != -1) tile[r * dp + cc[i]] = desc[r].w ? -vv[i] : vv[i];
   }
 }
 
-template <int G, typename IX, typename TV>
-__device__ __forceinline__ void unscatter_rows(TV *tile, int dp, int lane, const IX (&cc)[16]) {
+template <int G, typename TV>
+__device__ __forceinline__ void unscatter_rows(TV *tile, int dp, int lane, const int32_t (&cc)[16]) {
   constexpr int S = 32 / G;
   const int g = lane / G;
 #pragma unroll
   for (int i = 0; i < G; ++i)
-    if (cc[i] != (IX)-1) tile[(i * S + g) * dp + (int)cc[i]] = (TV)0;
+    if (cc[i] != -1) tile[(i * S + g) * dp + cc[i]] = (TV)0;
 }
 
 __device__ __forceinline__ int tile_g(int lmax) { return lmax <= 4 ? 4 : lmax <= 8 ? 8 : 16; }
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
     if (lane < nrows) descs[slot * 32 + lane] = make_int4((int)(uint32_t)rs, (int)(rs >> 32), len, (int)(wd >> 31));
     return tile_g(__reduce_max_sync(0xffffffffu, lane < nrows ? len : 0));
   };
-  auto load_sw = [&](int G, const int4 *dsc, int nrows, IX (&c)[16], TV (&v)[16]) {
+  auto load_sw = [&](int G, const int4 *dsc, int nrows, int32_t (&c)[16], TV (&v)[16]) {
     if (G == 4)
       load_rows<4>(dsc, nrows, aix, av, lane, c, v);
     else if (G == 8)
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
   // are requested into the same registers and stay in flight while batch b
   // is accumulated; the tile is cleared whole (no per-entry columns kept)
   int slot = 0;
-  IX cc[16];
+  int32_t cc[16];
   TV vv[16];
   int g0 = publish(slot, beg, rs0, len0, w0);
   __syncwarp();
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
   }
 #else
   int slot = 0;
-  IX c0[16], c1[16];
+  int32_t c0[16], c1[16];
   TV v0[16], v1[16];
   int g0 = publish(slot, beg, rs0, len0, w0);
   __syncwarp();

@@ -1,4 +1,5 @@
-"""The column-sweep kernel (csrc/csr_colsweep.cuh, skt_apply_csr_wide) for
+"""The wide-CSR kernels behind skt_apply_csr_wide (csrc/csr_colblock.cuh, the
+default, and csrc/csr_colsweep.cuh) for
 CSR A with SA rows too wide for on-chip accumulators (BASELINE config 5's
 shape): bit-exact against the oracle (sketch.py:155-164: per output, ascending
 row order from +0.0) on the edge cases of its design -- several column blocks
@@ -93,3 +94,31 @@ def test_colsweep_bucket_ranges():
     for b0, b1 in [(0, 1), (1, 17), (17, 40), (40, 41)]:
         op._apply_csr_device(ip, ix, vv, d, torch.float32, canonical=True, out=pieced, buckets=(b0, b1))
     assert torch.equal(pieced, full)
+
+
+_COLSWEEP_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from tests.test_gpu_wide import _check, _random_csr
+from paper_1207_6365_b200 import SparseEmbedding
+for n, d, t, per in [(3000, 70001, 37, 60), (5000, 30000, 2, 20)]:
+    rng = np.random.default_rng(n + d)
+    a = _random_csr(rng, n, d, per, np.float32)
+    _check(SparseEmbedding(n, t, 3), a, t, 3, d)
+print("ok")
+"""
+
+
+def test_colsweep_kernel_opt_in():
+    """The column-sweep kernel (SKT_CSR_WIDE=colsweep, csr_colsweep.cuh; the
+    default is csr_colblock.cuh), run in a child process (the selector is
+    read once per process): bit-exact against the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKT_CSR_WIDE="colsweep")
+    out = subprocess.run([sys.executable, "-c", _COLSWEEP_SCRIPT, root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
