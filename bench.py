@@ -415,6 +415,10 @@ def our_arm(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or (args.fused and "RANK" in os.environ):
+        # communicator lines on stderr (NCCL_DEBUG=INFO) so a scaling run shows
+        # every rank's device, transport (NVLink / NVLS) and ring layout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
         dist.init_process_group("nccl", device_id=dev)
     n, d, m = cfg["n"], cfg["d"], cfg["m"]
     # config 5 at N > 1: bucket ownership -- every rank holds the

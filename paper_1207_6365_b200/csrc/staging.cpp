@@ -4,12 +4,14 @@
 // ~11 GB/s on this platform against ~55 GB/s from page-locked memory
 // (tools/e2e_csr_probe.py), so skt_memcpy_staged pipelines the copy through a
 // ring of page-locked chunk buffers: host threads memcpy chunk i + 1 into a
-// free buffer while the DMA engine moves chunk i.  The ring (4 x 16 MB per
+// free buffer while the DMA engine moves chunk i.  The ring (8 x 4 MB per
 // device) and the worker threads are created on first use and reused.
 //
 //   kind 0 (H2D): returns once the source may be reused (the last DMAs are
 //                 stream-ordered before later work on `stream`);
 //   kind 1 (D2H): returns when dst holds the data (waits for the stream).
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -23,10 +25,13 @@
 namespace skt {
 namespace {
 
-constexpr size_t kChunk = 16u << 20;
-constexpr int kRing = 4;
+constexpr size_t kChunk = 4u << 20;
+constexpr int kRing = 8;
 
-// fixed pool of memcpy workers: parallel_copy splits one memcpy into slices
+// fixed pool of memcpy workers: copy() splits one memcpy into slices.  The
+// workers spin briefly on the task generation before sleeping, and the caller
+// spins on completion, so a chunk costs microseconds of hand-off, not a
+// condition-variable wake-up per worker.
 class CopyPool {
  public:
   CopyPool() {
@@ -35,9 +40,10 @@ class CopyPool {
     for (int i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { run(i); });
   }
   ~CopyPool() {
+    stop_.store(true);
     {
       std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
+      gen_.fetch_add(1);
     }
     cv_.notify_all();
     for (auto &t : workers_) t.join();
@@ -47,19 +53,18 @@ class CopyPool {
       std::memcpy(dst, src, bytes);
       return;
     }
-    std::unique_lock<std::mutex> call(call_m_);  // one parallel copy at a time
+    std::lock_guard<std::mutex> call(call_m_);  // one parallel copy at a time
+    dst_ = (char *)dst;
+    src_ = (const char *)src;
+    bytes_ = bytes;
+    pending_.store(nthreads_ - 1, std::memory_order_relaxed);
     {
       std::lock_guard<std::mutex> g(m_);
-      dst_ = (char *)dst;
-      src_ = (const char *)src;
-      bytes_ = bytes;
-      pending_ = nthreads_ - 1;
-      ++gen_;
+      gen_.fetch_add(1, std::memory_order_release);
     }
-    cv_.notify_all();
+    if (sleepers_.load() > 0) cv_.notify_all();
     slice(0);
-    std::unique_lock<std::mutex> g(m_);
-    done_cv_.wait(g, [this] { return pending_ == 0; });
+    while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
   }
 
  private:
@@ -71,24 +76,30 @@ class CopyPool {
   void run(int i) {
     uint64_t seen = 0;
     for (;;) {
-      {
+      // spin ~2 ms for the next task (back-to-back calls), then sleep
+      auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(2000))
+        std::this_thread::yield();
+      if (gen_.load(std::memory_order_acquire) == seen) {
         std::unique_lock<std::mutex> g(m_);
-        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
+        sleepers_.fetch_add(1);
+        cv_.wait(g, [&] { return gen_.load() != seen; });
+        sleepers_.fetch_sub(1);
       }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
       slice(i);
-      std::lock_guard<std::mutex> g(m_);
-      if (--pending_ == 0) done_cv_.notify_one();
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
   int nthreads_ = 1;
   std::vector<std::thread> workers_;
   std::mutex m_, call_m_;
-  std::condition_variable cv_, done_cv_;
-  bool stop_ = false;
-  uint64_t gen_ = 0;
-  int pending_ = 0;
+  std::condition_variable cv_;
+  std::atomic<bool> stop_{false};
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0}, sleepers_{0};
   char *dst_ = nullptr;
   const char *src_ = nullptr;
   size_t bytes_ = 0;

@@ -146,7 +146,7 @@ def _host(t: torch.Tensor) -> torch.Tensor:
     return out
 
 
-_STAGE_MIN = 4 << 20  # host arrays below this go through torch's own copy
+_STAGE_MIN = 1 << 20  # host arrays below this go through torch's own copy
 
 
 def _to_device(x: np.ndarray, device) -> torch.Tensor:
@@ -409,9 +409,14 @@ class SparseEmbedding(SketchOperator):
                 m = sp.csr_array(m, dtype=np.float64)
             dev = self.device
             ip, ix, vv = (_to_device(x, dev) for x in (m.indptr, m.indices, m.data))
-            # canonical form checked on the device (scipy's has_canonical_format
-            # is an O(nnz) host scan on every new csr object)
-            canonical = csr_is_canonical_device(ip, ix, m.shape[0])
+            # canonical form: scipy's cached flag when it has one (set by its
+            # conversions), else checked on the device (scipy's
+            # has_canonical_format is an O(nnz) host scan on every new object)
+            known = getattr(m, "_has_canonical_format", None)
+            if known is None:
+                known = csr_is_canonical_device(ip, ix, m.shape[0])
+                m.has_canonical_format = known  # cached on the object, as scipy's own check does
+            canonical = bool(known)
             return _host(self._apply_csr_device(ip, ix, vv, m.shape[1], out_t, canonical,
                                                 deterministic=deterministic)).numpy()
         arr = np.asarray(a)

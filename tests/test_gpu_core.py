@@ -681,11 +681,11 @@ def test_csr_check_sorted_device(rng):
         assert csr_is_canonical_device(ipz, ixz, 3)
 
 
-@pytest.mark.parametrize("nbytes", [1, 4_000_003, 16 << 20, (16 << 20) * 4 + 12345, (16 << 20) * 9 + 8])
+@pytest.mark.parametrize("nbytes", [1, 4_000_003, 4 << 20, (4 << 20) * 8 + 12345, (4 << 20) * 19 + 8, 123_456_789])
 def test_memcpy_staged_round_trip(nbytes):
     """skt_memcpy_staged (page-locked ring for pageable host memory): both
-    directions byte-exact for sizes below, at and across the 16 MB chunks and
-    the 4-buffer ring."""
+    directions byte-exact for sizes below, at and across the 4 MB chunks and
+    the 8-buffer ring."""
     host = np.frombuffer(np.random.default_rng(nbytes).bytes(nbytes), dtype=np.uint8).copy()
     dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
