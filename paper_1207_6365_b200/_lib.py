@@ -141,7 +141,7 @@ def lib() -> ctypes.CDLL:
         "skt_apply_csr": ([P, P, P, i32, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, u32, P], i32),
         "skt_memcpy_staged": ([P, P, sz, i32, P], i32),
         "skt_csr_check_sorted": ([i64, P, i32, P, i32, P, P], i32),
-        "skt_apply_csr_wide_workspace": ([i64, u64, i64, ctypes.POINTER(sz)], i32),
+        "skt_apply_csr_wide_workspace": ([i64, u64, i64, i64, i32, ctypes.POINTER(sz)], i32),
         "skt_apply_csr_wide": ([P, P, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, P, sz, P], i32),
         "skt_apply_dense_push": ([P, P, u64, i64, P, i32, i64, i64, i32, P, P, i32, i32, i64, i64, i64, P, P], i32),
         "skt_slot_sum": ([P, i32, i32, i64, i64, i64, i64, P, i64, P], i32),

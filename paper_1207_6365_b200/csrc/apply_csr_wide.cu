@@ -1,20 +1,17 @@
 // apply_csr_wide.cu -- K4 for CSR A too wide for on-chip accumulators of
-// whole SA rows: the column-sweep kernel (csr_colsweep.cuh) behind
+// whole SA rows: the partition path (csr_partition.cuh, default) and the
+// column-block kernel (csr_colblock.cuh, SKT_CSR_WIDE=colblock) behind
 // skt_apply_csr_wide (sketch.py:155-164, BASELINE config 5).
 #include <cstdlib>
 
 #include "common.cuh"
 #include "csr_colblock.cuh"
-#include "csr_colsweep.cuh"
+#include "csr_partition.cuh"
 
 namespace skt {
 namespace {
 
-// ---- column sweep (csr_colsweep.cuh): geometry and launch ------------------
-struct ColsweepGeom {
-  int nblk;
-  int64_t blk_cols;
-};
+// ---- wide CSR: launch ----------------------------------------------------
 inline int num_sms() {
   static const int n = [] {
     int dev = 0, v = kNumSMs;
@@ -23,25 +20,66 @@ inline int num_sms() {
   }();
   return n;
 }
-// column blocks per bucket: about 4 waves of 2 CTAs per SM, whole super-steps
-inline ColsweepGeom colsweep_geom(uint64_t t, int64_t d) {
-  const int64_t steps = std::max<int64_t>(1, (d + kCsStep - 1) / kCsStep);
-  const int64_t slots = 2LL * num_sms();
-  int64_t nblk = std::min<int64_t>(steps, std::max<int64_t>(1, (4 * slots + (int64_t)t - 1) / (int64_t)t));
-  const int64_t per = (steps + nblk - 1) / nblk;
-  nblk = (steps + per - 1) / per;
-  return ColsweepGeom{(int)nblk, per * kCsStep};
-}
 
-// SKT_CSR_WIDE=colsweep selects the column-sweep kernel (A/B)
-inline bool use_colsweep() {
-  static const bool on = [] {
+// SKT_CSR_WIDE=colblock selects the single-kernel column-block path (16 MB of
+// workspace for config 5 instead of the partition's ~nnz x 6 B; A/B)
+inline int wide_kernel() {
+  static const int k = [] {
     const char *e = getenv("SKT_CSR_WIDE");
-    return e && e[0] == 'c' && e[3] == 's';
+    return (e && e[0] == 'c') ? 1 : 2;  // 1 = colblock, 2 = partition (default)
   }();
-  return on;
+  return k;
 }
 inline int colblock_nblk(int64_t d) { return (int)std::max<int64_t>(1, (d + kCbCols - 1) / kCbCols); }
+
+struct PartLayout {
+  size_t np, pstart, pnz, pbase, reg, key, val, total;
+  int64_t maxpieces;
+};
+inline PartLayout part_layout(int64_t n, uint64_t t, int nblk, int64_t nnz, size_t vsize) {
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  PartLayout L;
+  L.maxpieces = n / kPtPiece + (int64_t)t + 1;  // sum over buckets of ceil(rows / piece)
+  L.np = 0;
+  L.pstart = L.np + up((size_t)t * 8);
+  L.pnz = L.pstart + up(((size_t)t + 1) * 8);
+  L.pbase = L.pnz + up((size_t)L.maxpieces * 8);
+  L.reg = L.pbase + up(((size_t)L.maxpieces + 1) * 8);
+  L.key = L.reg + up((size_t)L.maxpieces * (nblk + 1) * 8);
+  L.val = L.key + up((size_t)std::max<int64_t>(1, nnz) * 2);
+  L.total = L.val + up((size_t)std::max<int64_t>(1, nnz) * vsize);
+  return L;
+}
+
+template <typename IP, typename IX, typename TV, typename TOut>
+skt_status launch_partition(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
+                            const void *aix, const void *av, int64_t nnz, int64_t d, void *sa, int64_t ldsa,
+                            void *ws, cudaStream_t stream) {
+  static const char *fn = "skt_apply_csr_wide";
+  const int nblk = colblock_nblk(d);
+  const PartLayout L = part_layout(n, t, nblk, nnz, sizeof(TV));
+  char *w = (char *)ws;
+  int64_t *np = (int64_t *)(w + L.np), *pstart = (int64_t *)(w + L.pstart), *pnz = (int64_t *)(w + L.pnz);
+  int64_t *pbase = (int64_t *)(w + L.pbase), *reg = (int64_t *)(w + L.reg);
+  uint16_t *wkey = (uint16_t *)(w + L.key);
+  TV *wval = (TV *)(w + L.val);
+  SKT_LAUNCH(csr_part_npieces_kernel, (unsigned)((t + 255) / 256), 256, 0, stream, pindptr, t, np);
+  SKT_LAUNCH(csr_part_scan_kernel, 1, 1024, 0, stream, np, (int64_t)t, pstart);
+  SKT_LAUNCH((csr_part_piece_nnz_kernel<IP>), (unsigned)((L.maxpieces * 32 + 255) / 256), 256, 0, stream, pindptr,
+             prow, t, pstart, (const IP *)aip, pnz);
+  // pieces past the real count were not written: the scan reads pstart[t] of them
+  SKT_LAUNCH(csr_part_scan_kernel, 1, 1024, 0, stream, pnz, L.maxpieces, pbase);
+  auto ks = csr_part_scatter_kernel<IP, IX, TV>;
+  const int smem_s = (int)part_scatter_smem(nblk);
+  SKT_CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_s), fn);
+  SKT_LAUNCH(ks, (unsigned)L.maxpieces, kPtThreads, smem_s, stream, pindptr, prow, t, pstart, pbase, nblk,
+             (const IP *)aip, (const IX *)aix, (const TV *)av, reg, wkey, wval);
+  auto ka = csr_part_accum_kernel<TV, TOut>;
+  const int smem_a = (int)sizeof(PtSmem);
+  SKT_CUDA_TRY(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_a), fn);
+  SKT_LAUNCH(ka, (unsigned)(t * nblk), kPaThreads, smem_a, stream, nblk, d, pstart, reg, wkey, wval, (TOut *)sa, ldsa);
+  return check_launch(fn);
+}
 
 template <typename IP, typename IX, typename TV, typename TOut>
 skt_status launch_colblock(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
@@ -64,35 +102,23 @@ skt_status launch_colblock(const int64_t *pindptr, const uint32_t *prow, uint64_
 }
 
 template <typename IP, typename IX, typename TV, typename TOut>
-skt_status launch_colsweep(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
-                           const void *aix, const void *av, int64_t d, void *sa, int64_t ldsa, int32_t *cursor,
-                           cudaStream_t stream) {
-  static const char *fn = "skt_apply_csr_wide";
-  if (!use_colsweep()) return launch_colblock<IP, IX, TV, TOut>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, stream);
-  const ColsweepGeom g = colsweep_geom(t, d);
-  const int64_t items = (int64_t)n * g.nblk;
-  if (items > 0) {
-    SKT_LAUNCH((csr_colsweep_init_kernel<IP, IX>), (unsigned)((items + 255) / 256), 256, 0, stream, prow, n,
-               g.nblk, g.blk_cols, (const IP *)aip, (const IX *)aix, cursor);
-    SKT_CUDA_TRY(cudaGetLastError(), fn);
-  }
-  auto k = csr_colsweep_kernel<IP, IX, TV, TOut>;
-  const int smem = (int)sizeof(CsSmem);
-  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), fn);
-  SKT_LAUNCH(k, (unsigned)(t * g.nblk), kCsThreads, smem, stream, pindptr, prow, n, t, g.nblk, g.blk_cols, d,
-             (const IP *)aip, (const IX *)aix, (const TV *)av, cursor, (TOut *)sa, ldsa);
-  return check_launch(fn);
+skt_status launch_wide(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
+                       const void *aix, const void *av, int64_t nnz, int64_t d, void *sa, int64_t ldsa, void *ws,
+                       cudaStream_t stream) {
+  if (wide_kernel() == 2 && colblock_nblk(d) <= kPtMaxBlocks)
+    return launch_partition<IP, IX, TV, TOut>(pindptr, prow, t, n, aip, aix, av, nnz, d, sa, ldsa, ws, stream);
+  return launch_colblock<IP, IX, TV, TOut>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, (int32_t *)ws, stream);
 }
 
 template <typename IP, typename IX>
-skt_status colsweep_by_vals(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
-                            const void *aix, const void *av, skt_dtype vt, int64_t d, void *sa, skt_dtype ot,
-                            int64_t ldsa, int32_t *cursor, cudaStream_t s) {
+skt_status wide_by_vals(const int64_t *pindptr, const uint32_t *prow, uint64_t t, int64_t n, const void *aip,
+                            const void *aix, const void *av, skt_dtype vt, int64_t nnz, int64_t d, void *sa,
+                            skt_dtype ot, int64_t ldsa, int32_t *cursor, cudaStream_t s) {  // cursor: the workspace
   if (vt == SKT_F32)
-    return ot == SKT_F64 ? launch_colsweep<IP, IX, float, double>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, s)
-                         : launch_colsweep<IP, IX, float, float>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, s);
-  return ot == SKT_F64 ? launch_colsweep<IP, IX, double, double>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, s)
-                       : launch_colsweep<IP, IX, double, float>(pindptr, prow, t, n, aip, aix, av, d, sa, ldsa, cursor, s);
+    return ot == SKT_F64 ? launch_wide<IP, IX, float, double>(pindptr, prow, t, n, aip, aix, av, nnz, d, sa, ldsa, cursor, s)
+                         : launch_wide<IP, IX, float, float>(pindptr, prow, t, n, aip, aix, av, nnz, d, sa, ldsa, cursor, s);
+  return ot == SKT_F64 ? launch_wide<IP, IX, double, double>(pindptr, prow, t, n, aip, aix, av, nnz, d, sa, ldsa, cursor, s)
+                       : launch_wide<IP, IX, double, float>(pindptr, prow, t, n, aip, aix, av, nnz, d, sa, ldsa, cursor, s);
 }
 
 }  // namespace
@@ -100,11 +126,13 @@ skt_status colsweep_by_vals(const int64_t *pindptr, const uint32_t *prow, uint64
 
 using namespace skt;
 
-extern "C" skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, size_t *bytes) {
-  if (!bytes || n < 0 || t < 1 || d < 0) return fail(SKT_EINVAL, "skt_apply_csr_wide_workspace", "bad arguments");
-  const size_t sweep = (size_t)std::max<int64_t>(1, n) * (size_t)colsweep_geom(t, d).nblk * sizeof(int32_t);
+extern "C" skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, int64_t nnz, skt_dtype val_dtype,
+                                                   size_t *bytes) {
+  if (!bytes || n < 0 || t < 1 || d < 0 || nnz < 0 || (val_dtype != SKT_F32 && val_dtype != SKT_F64))
+    return fail(SKT_EINVAL, "skt_apply_csr_wide_workspace", "bad arguments");
   const size_t block = (size_t)std::max<int64_t>(1, n) * (size_t)std::max(1, colblock_nblk(d) - 1) * sizeof(int32_t);
-  *bytes = std::max(sweep, block);
+  const size_t part = part_layout(n, t, colblock_nblk(d), nnz, val_dtype == SKT_F32 ? 4 : 8).total;
+  *bytes = std::max(block, wide_kernel() == 2 && colblock_nblk(d) <= kPtMaxBlocks ? part : (size_t)0);
   return SKT_OK;
 }
 
@@ -122,15 +150,15 @@ extern "C" skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *
   if (d == 0) return SKT_OK;
   if (!sa || (n > 0 && !rows)) return fail(SKT_EINVAL, fn, "NULL buffer");
   size_t need = 0;
-  skt_apply_csr_wide_workspace(n, t, d, &need);
+  skt_apply_csr_wide_workspace(n, t, d, nnz, val_dtype, &need);
   if (!ws || ws_bytes < need) return fail(SKT_EWORKSPACE, fn, "workspace too small");
   cudaStream_t s = as_stream(stream_);
   int32_t *cur = (int32_t *)ws;
   if (indptr_type == SKT_I32)
     return index_type == SKT_I32
-               ? colsweep_by_vals<int32_t, int32_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, cur, s)
-               : colsweep_by_vals<int32_t, int64_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, cur, s);
+               ? wide_by_vals<int32_t, int32_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, cur, s)
+               : wide_by_vals<int32_t, int64_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, cur, s);
   return index_type == SKT_I32
-             ? colsweep_by_vals<int64_t, int32_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, cur, s)
-             : colsweep_by_vals<int64_t, int64_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, d, sa, sa_dtype, ldsa, cur, s);
+             ? wide_by_vals<int64_t, int32_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, cur, s)
+             : wide_by_vals<int64_t, int64_t>(indptr, rows, t, n, a_indptr, a_indices, a_vals, val_dtype, nnz, d, sa, sa_dtype, ldsa, cur, s);
 }

@@ -33,6 +33,7 @@ namespace {
 constexpr int kCbShift = 14;
 constexpr int kCbCols = 1 << kCbShift;  // 16384 columns per block
 constexpr int kCbThreads = 512;
+constexpr int kBndBatch = 9;  // bounds kernel: 288 column indices of a row in flight
 constexpr int kCbList = 2048;                   // entries of columns with >= 3 contributions
 constexpr int kCbChain = 32;                    // longest per-column chain sorted in registers
 constexpr int kCbRows = 2048;                   // row descriptors staged per chunk
@@ -52,14 +53,24 @@ __global__ void __launch_bounds__(256) csr_colblock_bounds_kernel(int64_t n, int
     const int64_t rs = (int64_t)aip[row], re = (int64_t)aip[row + 1];
     int32_t *o = bnd + row * nb1;
     int prevq = 0;  // block of the entry before this lane's
-    for (int64_t p0 = rs; p0 < re; p0 += 32) {
-      const int64_t p = p0 + lane;
-      const int q = p < re ? (int)((int64_t)__ldg(aix + p) >> kCbShift) : nblk;
-      const int qp = __shfl_up_sync(0xffffffffu, q, 1);
-      const int prev = lane == 0 ? prevq : qp;
-      // blocks (prev, q] start at this entry
-      for (int k = max(prev + 1, 1); k <= min(q, nb1); ++k) o[k - 1] = (int32_t)(p - rs);
-      prevq = __shfl_sync(0xffffffffu, q, 31);
+    for (int64_t b0 = rs; b0 < re; b0 += 32 * kBndBatch) {
+      int qs[kBndBatch];  // kBndBatch x 32 column indices in flight
+#pragma unroll
+      for (int j = 0; j < kBndBatch; ++j) {
+        const int64_t p = b0 + 32 * j + lane;
+        qs[j] = p < re ? (int)((int64_t)__ldg(aix + p) >> kCbShift) : nblk;
+      }
+#pragma unroll
+      for (int j = 0; j < kBndBatch; ++j) {
+        if (b0 + 32 * j >= re) break;  // warp-uniform
+        const int64_t p = b0 + 32 * j + lane;
+        const int q = qs[j];
+        const int qp = __shfl_up_sync(0xffffffffu, q, 1);
+        const int prev = lane == 0 ? prevq : qp;
+        // blocks (prev, q] start at this entry
+        for (int k = max(prev + 1, 1); k <= min(q, nb1); ++k) o[k - 1] = (int32_t)(p - rs);
+        prevq = __shfl_sync(0xffffffffu, q, 31);
+      }
     }
     // blocks after the row's last entry start at its end
     for (int k = max(prevq + 1, 1) + lane; k <= nb1; k += 32) o[k - 1] = (int32_t)(re - rs);

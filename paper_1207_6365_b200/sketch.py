@@ -507,7 +507,7 @@ class SparseEmbedding(SketchOperator):
         L = _lib.lib()
         m = self.row_end - self.row_begin
         nb = ctypes.c_size_t()
-        check(L.skt_apply_csr_wide_workspace(m, b1 - b0, d, ctypes.byref(nb)))
+        check(L.skt_apply_csr_wide_workspace(m, b1 - b0, d, vals.numel(), _TORCH_TO_SKT[vals.dtype], ctypes.byref(nb)))
         ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
         with torch.cuda.device(self.device):
             check(

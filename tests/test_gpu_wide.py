@@ -1,13 +1,13 @@
-"""The wide-CSR kernels behind skt_apply_csr_wide (csrc/csr_colblock.cuh, the
-default, and csrc/csr_colsweep.cuh) for
-CSR A with SA rows too wide for on-chip accumulators (BASELINE config 5's
-shape): bit-exact against the oracle (sketch.py:155-164: per output, ascending
-row order from +0.0) on the edge cases of its design -- several column blocks
-and a partial last super-step, buckets of more than 1024 rows (cursors in the
-workspace instead of shared memory), empty buckets and empty rows, rows with
-more than 16 entries in one 8192-column super-step (continuation loads), a
-column shared by every row of a bucket (same-column lanes serialised in row
-order), int64 index arrays, fp64 values, fp32 / fp64 output, bucket ranges."""
+"""The wide-CSR kernels behind skt_apply_csr_wide (csrc/csr_partition.cuh, the
+default; csrc/csr_colblock.cuh, opt-in) for CSR A with SA rows too wide for
+on-chip accumulators (BASELINE config 5's shape): bit-exact against the oracle
+(sketch.py:155-164: per output, ascending row order from +0.0) on the edge
+cases of their design -- several 16384-column blocks and a partial last one,
+buckets of more than 512 rows (several pieces), empty buckets and empty rows,
+rows with thousands of entries in one block, a column shared by every row of a
+bucket (chains longer than 32 and lists over 2048 entries: the ordered
+fallback), int64 index arrays, fp64 values, fp32 / fp64 output, bucket
+ranges."""
 
 import numpy as np
 import pytest
@@ -109,16 +109,18 @@ print("ok")
 """
 
 
-def test_colsweep_kernel_opt_in():
-    """The column-sweep kernel (SKT_CSR_WIDE=colsweep, csr_colsweep.cuh; the
-    default is csr_colblock.cuh), run in a child process (the selector is
-    read once per process): bit-exact against the oracle."""
+@pytest.mark.parametrize("kernel", ["colblock"])
+def test_wide_kernel_opt_in(kernel):
+    """The opt-in single-kernel wide path (SKT_CSR_WIDE=colblock:
+    csr_colblock.cuh; the default is the partition path, csr_partition.cuh),
+    run in a child process (the selector is read once per process): bit-exact
+    against the oracle."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SKT_CSR_WIDE="colsweep")
+    env = dict(os.environ, SKT_CSR_WIDE=kernel)
     out = subprocess.run([sys.executable, "-c", _COLSWEEP_SCRIPT, root], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
