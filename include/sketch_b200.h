@@ -134,10 +134,13 @@ skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, const uint
  * bit-identical result as skt_apply_csr (ascending row order per output from
  * +0.0), for CANONICAL input (sorted, distinct column indices per row: as_csr
  * output), shift-0 plan (indptr, rows).  One CTA per (bucket, column block)
- * sweeps 8192-column super-steps with fp64 accumulators in shared memory and
- * per-row cursors; no global atomics.  Workspace (device, caller-owned):
- * skt_apply_csr_wide_workspace(n, t, d) bytes -- the per-row cursors. */
-skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, size_t *bytes);
+ * accumulates 16384-column blocks with fp64 accumulators in shared memory
+ * after a stable partition of the bucket's entries by block; no global
+ * atomics.  Workspace (device, caller-owned): skt_apply_csr_wide_workspace(n,
+ * t, d, nnz, val_dtype) bytes -- row block boundaries and the partitioned
+ * entries (~nnz x (2 + value size) bytes). */
+skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, int64_t nnz, skt_dtype val_dtype,
+                                        size_t *bytes);
 skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
                               const void *a_indptr, skt_itype indptr_type, const void *a_indices,
                               skt_itype index_type, const void *a_vals, skt_dtype val_dtype, int64_t nnz,
