@@ -287,6 +287,77 @@ __global__ void __launch_bounds__(kPaThreads, 1) csr_part_accum_kernel(int nblk,
     S.overflow = ne >= (1LL << 31);
   }
   __syncthreads();
+  // register-resident fast path: the block's entries (<= kPaThreads x 2 x
+  // kPtItems) are loaded once, both sweeps work from registers
+  constexpr int kRes = 2 * kPtItems;
+  const bool resident = ne <= (int64_t)kPaThreads * kRes;
+  if (resident) {
+    int rc[kRes];
+    TV rv[kRes];
+    // entry u of this thread sits at position f(u) of the block's row order
+    auto fpos = [&](int u) -> int64_t {
+      return (int64_t)(u / kPtItems) * kPaThreads * kPtItems + (int64_t)tid * kPtItems + (u % kPtItems);
+    };
+    {
+      // flattened index f = chunk * (kPaThreads * kPtItems) + tid * kPtItems + j
+      int64_t posb = 0;
+#pragma unroll
+      for (int u = 0; u < kRes; ++u) rc[u] = -1;
+      for (int64_t jp = j0; jp < j1; ++jp) {
+        const int64_t s0 = reg[jp * (nblk + 1) + q], pn = reg[jp * (nblk + 1) + q + 1] - s0;
+#pragma unroll
+        for (int u = 0; u < kRes; ++u) {
+          const int64_t i = fpos(u) - posb;
+          if (i >= 0 && i < pn) {
+            rc[u] = (int)wkey[s0 + i];
+            rv[u] = wval[s0 + i];
+          }
+        }
+        posb += pn;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRes; ++u) {
+      const int c = rc[u];
+      if (c < 0) continue;
+      const uint32_t m = 1u << (c & 31);
+      if (atomicOr(&S.seen[0][c >> 5], m) & m)
+        if (atomicOr(&S.seen[1][c >> 5], m) & m) atomicOr(&S.seen[2][c >> 5], m);
+    }
+    __syncthreads();
+    for (int i = tid; i < kCbCols / 32; i += kPaThreads) {
+      uint32_t m = S.seen[1][i];
+      const uint32_t m3 = S.seen[2][i];
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        if (m3 & (1u << bit))
+          reinterpret_cast<long long *>(S.acc)[32 * i + bit] = -1LL;
+        else
+          S.acc[32 * i + bit] = 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kRes; ++u) {
+      const int c = rc[u];
+      if (c < 0) continue;
+      const double v = (double)rv[u];
+      const uint32_t m = 1u << (c & 31);
+      if (!(S.seen[1][c >> 5] & m)) {
+        S.acc[c] = v + 0.0;  // the reference's 0.0 + v
+      } else if (!(S.seen[2][c >> 5] & m)) {
+        atomicAdd(&S.acc[c], v);  // two adds from +0.0: order-free
+      } else {
+        const int slot = atomicAdd(&S.count, 1);
+        if (slot < kCbList) {
+          S.lpos[slot] = (int32_t)fpos(u);
+          S.lval[slot] = v;
+          S.lnext[slot] = (int32_t)atomicExch(reinterpret_cast<unsigned long long *>(S.acc) + c, (unsigned long long)slot);
+        }
+      }
+    }
+  } else {
   // ---- a. contributions per column (kPtItems consecutive keys per thread in flight)
   for (int64_t jp = j0; jp < j1; ++jp) {
   const int64_t s0 = reg[jp * (nblk + 1) + q], pn = reg[jp * (nblk + 1) + q + 1] - s0;
@@ -357,6 +428,7 @@ __global__ void __launch_bounds__(kPaThreads, 1) csr_part_accum_kernel(int nblk,
     }
   }
   posb += pn;
+  }
   }
   __syncthreads();
   if (S.count > kCbList) S.overflow = 1;
