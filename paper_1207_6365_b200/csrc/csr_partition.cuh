@@ -29,9 +29,10 @@ namespace {
 
 constexpr int kPtThreads = 512;
 constexpr int kPtPiece = 512;  // rows per piece
-constexpr int kPtBatch = 4;    // P3: 32-entry groups of a row in flight
+constexpr int kPtBatch = 9;    // P3: 32-entry groups of a row in flight (config 5: a whole row)
 constexpr int kPtItems = 8;    // P4: consecutive entries per thread per sweep step
 constexpr int kPaThreads = 1024;  // P4 threads
+constexpr int kPtPieceTab = 32;   // P4 register path: buckets of <= 32 pieces (16 K rows)
 constexpr int kPtMaxBlocks = 32;
 
 // P1a: pieces per bucket
@@ -254,6 +255,8 @@ inline size_t part_scatter_smem(int nblk) {
 struct PtSmem {
   double acc[kCbCols];
   uint32_t seen[3][kCbCols / 32];
+  int64_t pcum[kPtPieceTab];   // entries of the block before piece k (row order)
+  int64_t pslot[kPtPieceTab];  // workspace slot of piece k's block region
   int32_t lpos[kCbList];  // region position (= row rank order) of a >= 3 column's entry
   int32_t lnext[kCbList];
   double lval[kCbList];
@@ -285,12 +288,18 @@ __global__ void __launch_bounds__(kPaThreads, 1) csr_part_accum_kernel(int nblk,
   if (tid == 0) {
     S.count = 0;
     S.overflow = ne >= (1LL << 31);
+    int64_t acc = 0;
+    for (int64_t jp = j0; jp < j1 && jp - j0 < kPtPieceTab; ++jp) {
+      S.pcum[jp - j0] = acc;
+      S.pslot[jp - j0] = reg[jp * (nblk + 1) + q];
+      acc += reg[jp * (nblk + 1) + q + 1] - reg[jp * (nblk + 1) + q];
+    }
   }
   __syncthreads();
   // register-resident fast path: the block's entries (<= kPaThreads x 2 x
   // kPtItems) are loaded once, both sweeps work from registers
   constexpr int kRes = 2 * kPtItems;
-  const bool resident = ne <= (int64_t)kPaThreads * kRes;
+  const bool resident = ne <= (int64_t)kPaThreads * kRes && j1 - j0 <= kPtPieceTab;
   if (resident) {
     int rc[kRes];
     TV rv[kRes];
@@ -299,21 +308,20 @@ __global__ void __launch_bounds__(kPaThreads, 1) csr_part_accum_kernel(int nblk,
       return (int64_t)(u / kPtItems) * kPaThreads * kPtItems + (int64_t)tid * kPtItems + (u % kPtItems);
     };
     {
-      // flattened index f = chunk * (kPaThreads * kPtItems) + tid * kPtItems + j
-      int64_t posb = 0;
+      // pieces of the bucket: [S.pcum[k], S.pcum[k + 1]) of the block's row
+      // order start at workspace slot S.pslot[k] (tables built before the sweep)
+      const int np = (int)(j1 - j0);
 #pragma unroll
-      for (int u = 0; u < kRes; ++u) rc[u] = -1;
-      for (int64_t jp = j0; jp < j1; ++jp) {
-        const int64_t s0 = reg[jp * (nblk + 1) + q], pn = reg[jp * (nblk + 1) + q + 1] - s0;
-#pragma unroll
-        for (int u = 0; u < kRes; ++u) {
-          const int64_t i = fpos(u) - posb;
-          if (i >= 0 && i < pn) {
-            rc[u] = (int)wkey[s0 + i];
-            rv[u] = wval[s0 + i];
-          }
+      for (int u = 0; u < kRes; ++u) {
+        const int64_t f = fpos(u);
+        rc[u] = -1;
+        if (f < ne) {
+          int k = 0;
+          while (k + 1 < np && S.pcum[k + 1] <= f) ++k;
+          const int64_t i = S.pslot[k] + (f - S.pcum[k]);
+          rc[u] = (int)wkey[i];
+          rv[u] = wval[i];
         }
-        posb += pn;
       }
     }
 #pragma unroll
