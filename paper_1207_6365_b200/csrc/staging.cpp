@@ -69,7 +69,7 @@ class CopyPool {
 
  private:
   void slice(int i) {
-    const size_t per = (bytes_ / nthreads_ + 63) & ~(size_t)63;
+    const size_t per = ((bytes_ + nthreads_ - 1) / nthreads_ + 63) & ~(size_t)63;  // covers every byte
     const size_t b = std::min(bytes_, per * i), e = std::min(bytes_, per * (i + 1));
     if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
   }

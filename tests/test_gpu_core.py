@@ -681,7 +681,8 @@ def test_csr_check_sorted_device(rng):
         assert csr_is_canonical_device(ipz, ixz, 3)
 
 
-@pytest.mark.parametrize("nbytes", [1, 4_000_003, 4 << 20, (4 << 20) * 8 + 12345, (4 << 20) * 19 + 8, 123_456_789])
+@pytest.mark.parametrize("nbytes", [1, 1_600_004, 4_000_003, 4 << 20, (4 << 20) * 8 + 12345, (4 << 20) * 19 + 8,
+                                    123_456_789, (1 << 20) + 4])
 def test_memcpy_staged_round_trip(nbytes):
     """skt_memcpy_staged (page-locked ring for pageable host memory): both
     directions byte-exact for sizes below, at and across the 4 MB chunks and
