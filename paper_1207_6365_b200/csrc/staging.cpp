@@ -20,6 +20,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "common.cuh"
 
 namespace skt {
@@ -34,7 +36,7 @@ constexpr int kRing = 8;
 // condition-variable wake-up per worker.
 class CopyPool {
  public:
-  CopyPool() {
+  CopyPool() : pid_(getpid()) {
     unsigned hw = std::thread::hardware_concurrency();
     nthreads_ = (int)std::max(1u, std::min(8u, hw > 1 ? hw / 2 : 1u));
     for (int i = 1; i < nthreads_; ++i) workers_.emplace_back([this, i] { run(i); });
@@ -49,7 +51,8 @@ class CopyPool {
     for (auto &t : workers_) t.join();
   }
   void copy(void *dst, const void *src, size_t bytes) {
-    if (bytes < (1u << 20) || nthreads_ == 1) {
+    // a fork()ed child has none of the workers: copy on the calling thread
+    if (bytes < (1u << 20) || nthreads_ == 1 || getpid() != pid_) {
       std::memcpy(dst, src, bytes);
       return;
     }
@@ -94,6 +97,7 @@ class CopyPool {
     }
   }
   int nthreads_ = 1;
+  pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex m_, call_m_;
   std::condition_variable cv_;
