@@ -147,6 +147,33 @@ skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint6
                               int64_t d, void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* Row-window kernel for canonical CSR (csrc/csr_window.cuh): the same contract
+ * and bit-identical result as skt_apply_csr, for fp32 values / int32 column
+ * indices with rows of about 16 stored entries and an m x d fp64 SA that fits
+ * the chip's shared memory (BASELINE config 4).  A is streamed ONCE in row
+ * order: rows are cut into windows of W consecutive rows, every row of a
+ * window is written as one 128-byte slot at its rank in the window's stable
+ * sort by bucket (an L2-resident ring of windows), and the warp owning a
+ * bucket range adds its contiguous slot range in ascending row order into
+ * shared-memory fp64 accumulators.  No global data atomics.
+ *   skt_csr_window_config: W (rows per window, 0 = shape not supported on this
+ *     device) and the window count for an n-row input.
+ *   skt_plan_window_build: from the shift-0 plan (indptr, rows) of
+ *     skt_plan_build: pos[n] (slot of each row inside its window | sign << 31)
+ *     and wpi[n_windows][t + 1] (first slot of every bucket per window).
+ *   skt_apply_csr_window: SA (t x d, ldsa) in sa_dtype; SKT_ENOTSUP when the
+ *     shape / alignment is outside the kernel's range (call skt_apply_csr). */
+skt_status skt_csr_window_config(int64_t n, uint64_t t, int64_t d, int32_t *rows_per_window,
+                                 int32_t *n_windows);
+skt_status skt_plan_window_build(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,
+                                 int32_t rows_per_window, uint32_t *pos, int32_t *wpi, void *stream);
+skt_status skt_apply_csr_window_workspace(int64_t n, int32_t rows_per_window, size_t *bytes);
+skt_status skt_apply_csr_window(const uint32_t *pos, const int32_t *wpi, int32_t rows_per_window,
+                                uint64_t t, int64_t n, const void *a_indptr, skt_itype indptr_type,
+                                const int32_t *a_indices, const float *a_vals, int64_t nnz, int64_t d,
+                                void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws, size_t ws_bytes,
+                                void *stream);
+
 /* skt_memcpy_staged: copy between PAGEABLE host memory and the device through
  * a ring of page-locked chunk buffers (host memcpy of chunk i + 1 overlaps the
  * DMA of chunk i; the CUDA driver copies pageable memory at ~11 GB/s here,

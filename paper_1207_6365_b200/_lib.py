@@ -42,6 +42,10 @@ EXPORTS = (
     "skt_csr_check_sorted",
     "skt_apply_csr_wide_workspace",
     "skt_apply_csr_wide",
+    "skt_csr_window_config",
+    "skt_plan_window_build",
+    "skt_apply_csr_window_workspace",
+    "skt_apply_csr_window",
     "skt_apply_dense_push",
     "skt_slot_sum",
     "skt_apply_right_dense",
@@ -143,6 +147,10 @@ def lib() -> ctypes.CDLL:
         "skt_csr_check_sorted": ([i64, P, i32, P, i32, P, P], i32),
         "skt_apply_csr_wide_workspace": ([i64, u64, i64, i64, i32, ctypes.POINTER(sz)], i32),
         "skt_apply_csr_wide": ([P, P, u64, i64, P, i32, P, i32, P, i32, i64, i64, P, i32, i64, P, sz, P], i32),
+        "skt_csr_window_config": ([i64, u64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+        "skt_plan_window_build": ([P, P, u64, i64, i32, P, P, P], i32),
+        "skt_apply_csr_window_workspace": ([i64, i32, ctypes.POINTER(sz)], i32),
+        "skt_apply_csr_window": ([P, P, i32, u64, i64, P, i32, P, P, i64, i64, P, i32, i64, P, sz, P], i32),
         "skt_apply_dense_push": ([P, P, u64, i64, P, i32, i64, i64, i32, P, P, i32, i32, i64, i64, i64, P, P], i32),
         "skt_slot_sum": ([P, i32, i32, i64, i64, i64, i64, P, i64, P], i32),
         "skt_apply_right_dense": ([P, P, u64, i64, i64, P, i32, i64, P, i32, i64, P, P], i32),

@@ -324,6 +324,60 @@ class SparseEmbedding(SketchOperator):
                     self._grouped_ws = ws
             return self._grouped[shift]
 
+    def window_plan(self, d: int):
+        """Plan of the row-window CSR kernel (csrc/csr_window.cuh): ``(W, pos,
+        wpi)`` -- rows per window, every row's slot inside its window (sign in
+        bit 31) and the first slot of every bucket per window -- or None when
+        (t, d) is outside the kernel's range on this device.  Built once from
+        the per-bucket plan and cached."""
+        L = _lib.lib()
+        m = self.row_end - self.row_begin
+        w, nwin = ctypes.c_int32(), ctypes.c_int32()
+        with torch.cuda.device(self.device):
+            check(L.skt_csr_window_config(m, self.output_dim, d, ctypes.byref(w), ctypes.byref(nwin)))
+        if w.value == 0:
+            return None
+        with self._plan_lock:
+            cached = getattr(self, "_window", None)
+            if cached is None or cached[0] != w.value:
+                pos = torch.empty(m, dtype=torch.int32, device=self.device)
+                wpi = torch.empty((nwin.value, self.output_dim + 1), dtype=torch.int32, device=self.device)
+                with torch.cuda.device(self.device):
+                    check(L.skt_plan_window_build(_ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim,
+                                                  m, w.value, _ptr(pos), _ptr(wpi), _stream_ptr(self.device)))
+                self._window = cached = (w.value, pos, wpi)
+            return cached
+
+    def _window_eligible(self, indptr, indices, vals, d: int, nnz: int) -> bool:
+        """The row-window kernel is opt-in (``SKT_CSR_WINDOW=1``): bit-identical,
+        but measured slower than csr_tile on config 4 (0.50 vs 0.26 ms, DESIGN.md
+        section 4).  It takes fp32 values, int32 column indices and 16-byte
+        aligned arrays."""
+        if os.environ.get("SKT_CSR_WINDOW", "0") != "1":
+            return False
+        if vals.dtype != torch.float32 or indices.dtype != torch.int32:
+            return False
+        if any(x.data_ptr() % 16 for x in (vals, indices, indptr)):
+            return False
+        return self.row_end - self.row_begin > 0
+
+    def _apply_csr_window(self, plan, indptr, indices, vals, d: int, out):
+        L = _lib.lib()
+        w, pos, wpi = plan
+        m = self.row_end - self.row_begin
+        nb = ctypes.c_size_t()
+        check(L.skt_apply_csr_window_workspace(m, w, ctypes.byref(nb)))
+        ws = torch.empty(nb.value, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            check(
+                L.skt_apply_csr_window(
+                    _ptr(pos), _ptr(wpi), w, self.output_dim, m, _ptr(indptr), _ITYPE[indptr.dtype],
+                    _ptr(indices), _ptr(vals), vals.numel(), d, _ptr(out), _TORCH_TO_SKT[out.dtype],
+                    max(out.stride(0), 1), _ptr(ws), nb.value, _stream_ptr(self.device),
+                )
+            )
+        return out
+
     def csr_group_shift(self, d: int, canonical: bool, nnz: int | None = None) -> int:
         """Plan granularity for the CSR kernels.  Short canonical rows (mean
         <= 8 nonzeros) use the grouped sweep: 2^shift buckets per warp, about
@@ -483,6 +537,12 @@ class SparseEmbedding(SketchOperator):
             # wide SA rows (config 5): the column-sweep kernel, shared-memory
             # fp64 accumulators per 8192-column super-step, no global atomics
             return self._apply_csr_wide(indptr, indices, vals, d, out, b0, b1)
+        if (shift is None and deterministic and canonical and b0 == 0 and b1 == self.output_dim and d > 0
+                and self._window_eligible(indptr, indices, vals, d, vals.numel())):
+            # opt-in: A streamed once in row order (csr_window.cuh)
+            plan = self.window_plan(d)
+            if plan is not None:
+                return self._apply_csr_window(plan, indptr, indices, vals, d, out)
         if shift is None:
             shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
         if b0 % (1 << shift):
