@@ -174,6 +174,24 @@ skt_status skt_apply_csr_window(const uint32_t *pos, const int32_t *wpi, int32_t
                                 void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws, size_t ws_bytes,
                                 void *stream);
 
+/* Window gather kernel for canonical CSR (csrc/csr_cta.cuh): same contract and
+ * bit-identical result as skt_apply_csr, fp32 values / int32 column indices,
+ * m x d fp64 accumulators within the chip's shared memory.  Every SM owns a
+ * contiguous bucket range; all SMs walk A window by window (rows of a window
+ * stably sorted by bucket: wrows = the inverse of skt_plan_window_build's pos,
+ * with the same wpi), loader warps gather the SM's rows of the window into
+ * shared-memory slots with cp.async, accumulating half warps add them in
+ * ascending row order.  No global workspace, no atomics.
+ *   skt_csr_cta_config: rows per window (0 = shape not supported) and windows.
+ *   skt_plan_window_rows: wrows[n] from pos[n] (same rows_per_window). */
+skt_status skt_csr_cta_config(int64_t n, uint64_t t, int64_t d, int32_t *rows_per_window, int32_t *n_windows);
+skt_status skt_plan_window_rows(const uint32_t *pos, int64_t n, int32_t rows_per_window, uint32_t *wrows,
+                                void *stream);
+skt_status skt_apply_csr_cta(const uint32_t *wrows, const int32_t *wpi, int32_t rows_per_window, uint64_t t,
+                             int64_t n, const void *a_indptr, skt_itype indptr_type, const int32_t *a_indices,
+                             const float *a_vals, int64_t nnz, int64_t d, void *sa, skt_dtype sa_dtype,
+                             int64_t ldsa, void *stream);
+
 /* skt_memcpy_staged: copy between PAGEABLE host memory and the device through
  * a ring of page-locked chunk buffers (host memcpy of chunk i + 1 overlaps the
  * DMA of chunk i; the CUDA driver copies pageable memory at ~11 GB/s here,

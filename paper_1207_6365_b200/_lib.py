@@ -46,6 +46,9 @@ EXPORTS = (
     "skt_plan_window_build",
     "skt_apply_csr_window_workspace",
     "skt_apply_csr_window",
+    "skt_csr_cta_config",
+    "skt_plan_window_rows",
+    "skt_apply_csr_cta",
     "skt_apply_dense_push",
     "skt_slot_sum",
     "skt_apply_right_dense",
@@ -151,6 +154,9 @@ def lib() -> ctypes.CDLL:
         "skt_plan_window_build": ([P, P, u64, i64, i32, P, P, P], i32),
         "skt_apply_csr_window_workspace": ([i64, i32, ctypes.POINTER(sz)], i32),
         "skt_apply_csr_window": ([P, P, i32, u64, i64, P, i32, P, P, i64, i64, P, i32, i64, P, sz, P], i32),
+        "skt_csr_cta_config": ([i64, u64, i64, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+        "skt_plan_window_rows": ([P, i64, i32, P, P], i32),
+        "skt_apply_csr_cta": ([P, P, i32, u64, i64, P, i32, P, P, i64, i64, P, i32, i64, P], i32),
         "skt_apply_dense_push": ([P, P, u64, i64, P, i32, i64, i64, i32, P, P, i32, i32, i64, i64, i64, P, P], i32),
         "skt_slot_sum": ([P, i32, i32, i64, i64, i64, i64, P, i64, P], i32),
         "skt_apply_right_dense": ([P, P, u64, i64, i64, P, i32, i64, P, i32, i64, P, P], i32),

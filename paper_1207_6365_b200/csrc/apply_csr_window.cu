@@ -5,6 +5,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "csr_cta.cuh"
 #include "csr_window.cuh"
 
 namespace skt {
@@ -152,3 +153,79 @@ extern "C" skt_status skt_apply_csr_window(const uint32_t *pos, const int32_t *w
                              : win_launch<int64_t, float>(p, chunks, G, smem, s);
 }
 
+
+// ---- window gather kernel (csr_cta.cuh) -----------------------------------
+namespace {
+size_t cta_smem_bytes(uint64_t t, int64_t d, int G, int *bpc_out) {
+  if (G <= 0 || d < 1 || d >= (1 << 20)) return 0;
+  const int64_t bpc = ((int64_t)t + G - 1) / G;
+  if (bpc > 16 * kCtaAcc) return 0;  // <= 8 buckets per accumulating half warp
+  const size_t bytes = (size_t)kCtaBufs * kCtaRing * (128 + 4) + (size_t)bpc * d * 8;
+  if (bytes > 226 * 1024) return 0;
+  *bpc_out = (int)bpc;
+  return bytes;
+}
+}  // namespace
+
+extern "C" skt_status skt_csr_cta_config(int64_t n, uint64_t t, int64_t d, int32_t *rows_per_window,
+                                         int32_t *n_windows) {
+  static const char *fn = "skt_csr_cta_config";
+  if (!rows_per_window || !n_windows || n < 0 || t < 1) return fail(SKT_EINVAL, fn, "bad arguments");
+  *rows_per_window = 0;
+  *n_windows = 0;
+  const int G = win_sms();
+  int bpc;
+  if (n < 1 || n >= (1LL << 31) || t > (1ull << 31) || cta_smem_bytes(t, d, G, &bpc) == 0) return SKT_OK;
+  int rpc = win_env("SKT_CTA_ROWS", 512);  // mean rows per CTA and window
+  if (rpc < 32 || rpc > 1 << 16) rpc = 512;
+  const int64_t W = (int64_t)G * rpc;
+  *rows_per_window = (int32_t)W;
+  *n_windows = (int32_t)((n + W - 1) / W);
+  return SKT_OK;
+}
+
+extern "C" skt_status skt_plan_window_rows(const uint32_t *pos, int64_t n, int32_t W, uint32_t *wrows,
+                                           void *stream_) {
+  static const char *fn = "skt_plan_window_rows";
+  if (!pos || !wrows || n < 1 || n >= (1LL << 31) || W < 32) return fail(SKT_EINVAL, fn, "bad arguments");
+  SKT_LAUNCH(win_rows_kernel, (unsigned)((n + 255) / 256), 256, 0, as_stream(stream_), pos, n, W, wrows);
+  return check_launch(fn);
+}
+
+extern "C" skt_status skt_apply_csr_cta(const uint32_t *wrows, const int32_t *wpi, int32_t W, uint64_t t, int64_t n,
+                                        const void *a_indptr, skt_itype indptr_type, const int32_t *a_indices,
+                                        const float *a_vals, int64_t nnz, int64_t d, void *sa, skt_dtype sa_dtype,
+                                        int64_t ldsa, void *stream_) {
+  static const char *fn = "skt_apply_csr_cta";
+  if (!wrows || !wpi || !a_indptr || !sa || t < 1 || n < 1 || n >= (1LL << 31) || nnz < 0 || d < 1 || ldsa < d ||
+      W < 32 || (indptr_type != SKT_I32 && indptr_type != SKT_I64) ||
+      (sa_dtype != SKT_F32 && sa_dtype != SKT_F64) || (nnz > 0 && (!a_indices || !a_vals)))
+    return fail(SKT_EINVAL, fn, "bad arguments");
+  const int G = win_sms();
+  int bpc = 0;
+  const size_t smem = cta_smem_bytes(t, d, G, &bpc);
+  if (smem == 0) return fail(SKT_ENOTSUP, fn, "shape not supported by the window gather kernel");
+  CtaParams p;
+  p.aip = a_indptr;
+  p.aix = a_indices;
+  p.av = a_vals;
+  p.n = n;
+  p.d = (int)d;
+  p.dp = (int)d;
+  p.t = t;
+  p.wrows = wrows;
+  p.wpi = wpi;
+  p.W = W;
+  p.nwin = (int32_t)((n + W - 1) / W);
+  p.bpc = bpc;
+  p.sa = sa;
+  p.ldsa = ldsa;
+  cudaStream_t s = as_stream(stream_);
+  typedef void (*KFn)(const CtaParams);
+  const KFn k = indptr_type == SKT_I32
+                    ? (sa_dtype == SKT_F64 ? (KFn)csr_cta_kernel<int32_t, double> : (KFn)csr_cta_kernel<int32_t, float>)
+                    : (sa_dtype == SKT_F64 ? (KFn)csr_cta_kernel<int64_t, double> : (KFn)csr_cta_kernel<int64_t, float>);
+  SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+  SKT_LAUNCH(k, (unsigned)G, kCtaThreads, smem, s, p);
+  return check_launch(fn);
+}

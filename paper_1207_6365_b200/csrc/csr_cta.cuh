@@ -36,11 +36,17 @@ namespace skt {
 namespace {
 
 constexpr int kCtaLoad = 8;    // loader warps
-constexpr int kCtaAcc = 12;    // accumulating warps (24 half warps)
+constexpr int kCtaAcc = 16;    // accumulating warps (32 half warps)
 constexpr int kCtaThreads = (kCtaLoad + kCtaAcc) * 32;
-constexpr int kCtaRing = 576;  // rows per round (slots of one buffer)
-constexpr int kCtaBufs = 2;
-constexpr int kCtaChunks = kCtaRing / 32;                            // 18 chunks of 32 rows per round
+#ifndef SKT_CTA_RING
+#define SKT_CTA_RING 288
+#endif
+#ifndef SKT_CTA_BUFS
+#define SKT_CTA_BUFS 4
+#endif
+constexpr int kCtaRing = SKT_CTA_RING;  // rows per round (slots of one buffer), a multiple of 32
+constexpr int kCtaBufs = SKT_CTA_BUFS;
+constexpr int kCtaChunks = kCtaRing / 32;                            // chunks of 32 rows per round
 constexpr int kCtaCpl = (kCtaChunks + kCtaLoad - 1) / kCtaLoad;      // chunks per loader warp and round
 constexpr uint32_t kCtaLong = 0xffu;
 
@@ -79,6 +85,33 @@ __device__ __forceinline__ void ct_cp4(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ct_lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 ct_lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double ct_ldsf64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+// acc[a] += v when on (one predicated load / add / store, no branch)
+__device__ __forceinline__ void ct_acc_add(uint32_t a, double v, bool on) {
+  asm volatile(
+      "{ .reg .pred p; .reg .f64 t; setp.ne.u32 p, %2, 0; @p ld.shared.f64 t, [%0]; @p add.f64 t, t, %1; "
+      "@p st.shared.f64 [%0], t; }" ::"r"(a),
+      "d"(v), "r"((uint32_t)on)
+      : "memory");
+}
+__device__ __forceinline__ void ct_stsf64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
 // The CTA's rounds: window w contributes its rank range [lo_w, hi_w) cut into
 // pieces of <= kCtaRing rows.  Both roles step through the same sequence.
 struct CtaRounds {
@@ -86,6 +119,7 @@ struct CtaRounds {
   uint64_t t;
   int64_t b_lo, b_hi;  // the CTA's buckets
   int nwin, w, r0, hi;
+  int nlo, nhi;  // the next window's range, loaded one window ahead
   __device__ void range(int win, int &lo, int &h) const {
     lo = h = 0;
     if (win < nwin && b_lo < b_hi) {
@@ -96,12 +130,15 @@ struct CtaRounds {
   __device__ void start() {
     w = 0;
     range(0, r0, hi);
+    range(1, nlo, nhi);
     skip_empty();
   }
   __device__ void skip_empty() {
     while (w < nwin && r0 >= hi) {
       ++w;
-      range(w, r0, hi);
+      r0 = nlo;
+      hi = nhi;
+      range(w + 1, nlo, nhi);
     }
   }
   __device__ bool done() const { return w >= nwin; }
@@ -149,34 +186,45 @@ __global__ void __launch_bounds__(kCtaThreads, 1) csr_cta_kernel(const CtaParams
     // ------------------------------------------------------------ loaders
     typedef typename std::conditional<sizeof(IP) == 4, int32_t, int64_t>::type E;
     const int g = lane >> 4, gl = lane & 15;
-    // descriptors of this warp's chunks (chunk j = warp + kCtaLoad * k of the round), lane = row
-    uint32_t wr_c[kCtaCpl];
-    E rs_c[kCtaCpl];
-    int len_c[kCtaCpl];
-    auto load_desc = [&](const CtaRounds &r, uint32_t (&wr)[kCtaCpl], E (&rs)[kCtaCpl], int (&len)[kCtaCpl]) {
+    // This warp's chunks of a round: chunk warp + kCtaLoad * k, lane = row.
+    // Plan words are loaded two rounds ahead, indptr pairs one round ahead.
+    constexpr uint32_t kNoRow = 0xffffffffu;
+    auto load_rows = [&](const CtaRounds &r, uint32_t (&wr)[kCtaCpl]) {
 #pragma unroll
       for (int k = 0; k < kCtaCpl; ++k) {
-        wr[k] = 0;
-        rs[k] = 0;
-        len[k] = -1;  // no row
+        wr[k] = kNoRow;
         if (!r.done()) {
           const int rank = r.r0 + 32 * (warp + kCtaLoad * k) + lane;
-          if (rank < r.r1()) {
-            wr[k] = __ldg(p.wrows + (size_t)r.w * p.W + rank);
-            const int64_t row = wr[k] & 0x7fffffffu;
-            rs[k] = (E)aip[row];
-            len[k] = (int)((E)aip[row + 1] - rs[k]);
-          }
+          if (rank < r.r1()) wr[k] = __ldg(p.wrows + (size_t)r.w * p.W + rank);
         }
       }
     };
-    load_desc(it, wr_c, rs_c, len_c);
+    auto load_aip = [&](const uint32_t (&wr)[kCtaCpl], E (&rs)[kCtaCpl], int (&len)[kCtaCpl]) {
+#pragma unroll
+      for (int k = 0; k < kCtaCpl; ++k) {
+        rs[k] = 0;
+        len[k] = -1;  // no row
+        if (wr[k] != kNoRow) {
+          const int64_t row = wr[k] & 0x7fffffffu;
+          rs[k] = (E)aip[row];
+          len[k] = (int)((E)aip[row + 1] - rs[k]);
+        }
+      }
+    };
+    CtaRounds n1 = it;
+    n1.next();
+    CtaRounds n2 = n1;
+    n2.next();
+    uint32_t wr_c[kCtaCpl], wr_n[kCtaCpl];
+    E rs_c[kCtaCpl];
+    int len_c[kCtaCpl];
+    load_rows(it, wr_c);
+    load_rows(n1, wr_n);
+    load_aip(wr_c, rs_c, len_c);
     uint32_t q = 0;
     while (!it.done()) {
-      const int buf = q & 1;
-      const uint32_t ph = (q >> 1) & 1u;
-      CtaRounds nx = it;
-      nx.next();
+      const int buf = q % kCtaBufs;
+      const uint32_t ph = (q / kCtaBufs) & 1u;
       ct_mbar_wait(&empty[buf], ph ^ 1u);
       const uint32_t sbase = ct_smem(slots + (size_t)buf * kCtaRing * 128);
       uint32_t *mb = meta + buf * kCtaRing;
@@ -211,8 +259,15 @@ __global__ void __launch_bounds__(kCtaThreads, 1) csr_cta_kernel(const CtaParams
       ct_mbar_arrive_cpasync(&full[buf]);  // fires when this thread's copies have landed
       __syncwarp();
       if (lane == 0) ct_mbar_arrive(&full[buf]);  // releases the meta words
-      load_desc(nx, wr_c, rs_c, len_c);           // next round's descriptors, in flight during this round
-      it = nx;
+      // rotate: next round's indptr pairs (its plan words arrived a round ago),
+      // the round after's plan words
+#pragma unroll
+      for (int k = 0; k < kCtaCpl; ++k) wr_c[k] = wr_n[k];
+      load_aip(wr_c, rs_c, len_c);
+      load_rows(n2, wr_n);
+      it = n1;
+      n1 = n2;
+      n2.next();
       ++q;
     }
   } else {
@@ -222,23 +277,28 @@ __global__ void __launch_bounds__(kCtaThreads, 1) csr_cta_kernel(const CtaParams
     const int h = aw * 2 + half;  // this half warp's buckets: h, h + 2A, ...
     constexpr int kHalves = 2 * kCtaAcc;
     const int nbk = (int)(it.b_hi - it.b_lo);
+    const int kmax = (nbk + kHalves - 1) / kHalves;  // <= 8 (the host checks bpc)
     uint32_t q = 0;
-    int w_offs = -1;
-    // bucket offsets of the current window: lane k of the half warp holds
-    // off[b_k] (k even slot) ... kept simple: re-read per bucket from global (L2-resident, 2 MB)
     while (!it.done()) {
-      const int buf = q & 1;
-      const uint32_t ph = (q >> 1) & 1u;
+      const int buf = q % kCtaBufs;
+      const uint32_t ph = (q / kCtaBufs) & 1u;
       const int r0 = it.r0, r1 = it.r1();
       const int32_t *wp = p.wpi + (size_t)it.w * (p.t + 1) + it.b_lo;
-      (void)w_offs;
+      // rank bounds of this half warp's buckets: lane 2k holds off[b_k], lane 2k+1 off[b_k + 1]
+      int offv = 0;
+      {
+        const int kk = j >> 1, b = h + kHalves * kk;
+        if (kk < kmax && b < nbk) offv = __ldg(wp + b + (j & 1));
+      }
       ct_mbar_wait(&full[buf], ph);
       const unsigned char *sb = slots + (size_t)buf * kCtaRing * 128;
-      const uint32_t *mb = meta + buf * kCtaRing;
-      for (int b = h; b < nbk + kHalves; b += kHalves) {  // uniform trip count per warp
+      const uint32_t sb_u = ct_smem(sb) + j * 8, mb_u = ct_smem(meta + buf * kCtaRing), acc_u = ct_smem(acc);
+      for (int kk = 0; kk < kmax; ++kk) {
+        const int b = h + kHalves * kk;
+        const int o0 = __shfl_sync(0xffffffffu, offv, (lane & 16) + 2 * kk);
+        const int o1 = __shfl_sync(0xffffffffu, offv, (lane & 16) + 2 * kk + 1);
         int s0 = 0, s1 = 0;
         if (b < nbk) {
-          const int o0 = __ldg(wp + b), o1 = __ldg(wp + b + 1);
           s0 = (o0 > r0 ? o0 : r0) - r0;
           s1 = (o1 < r1 ? o1 : r1) - r0;
           if (s1 < s0) s1 = s0;
@@ -246,26 +306,35 @@ __global__ void __launch_bounds__(kCtaThreads, 1) csr_cta_kernel(const CtaParams
         const int mylen = s1 - s0;
         const int other = __shfl_xor_sync(0xffffffffu, mylen, 16);
         const int steps = mylen > other ? mylen : other;
-        double *ab = acc + (size_t)(b < nbk ? b : 0) * dp;
+        const uint32_t ab_u = acc_u + (uint32_t)(b < nbk ? b : 0) * (uint32_t)dp * 8u;
+        uint32_t ma = mb_u + (uint32_t)s0 * 4u, sa_u = sb_u + (uint32_t)s0 * 128u;
+        // the next row's meta word and entry are fetched one step ahead
+        const int last = mylen > 0 ? mylen - 1 : 0;
+        uint32_t m_n = ct_lds32(ma);
+        uint2 e_n = ct_lds64(sa_u);
         for (int r = 0; r < steps; ++r) {
-          if (r < mylen) {
-            const int s = s0 + r;
-            const uint32_t m = mb[s];
-            const uint32_t len = m & 0xffu;
-            const bool neg = (m >> 8) != 0;
-            if (len != kCtaLong) {
-              if ((uint32_t)j < len) {
-                const uint2 e = *reinterpret_cast<const uint2 *>(sb + (size_t)s * 128 + j * 8);
-                const double v = (double)__uint_as_float(e.y ^ (neg ? 0x80000000u : 0u));
-                ab[e.x] += v;
-              }
-            } else {  // a row longer than a slot: straight from A, 16 entries per step
-              const uint32_t *sl = reinterpret_cast<const uint32_t *>(sb + (size_t)s * 128);
+          const uint32_t m = m_n;
+          const uint2 e = e_n;
+          {  // unconditional (clamped) loads: no branch inside the step
+            const uint32_t rn = (uint32_t)(r + 1 < mylen ? r + 1 : last);
+            m_n = ct_lds32(ma + 4u * rn);
+            e_n = ct_lds64(sa_u + 128u * rn);
+          }
+          const uint32_t len = m & 0xffu;
+          const bool live = r < mylen;
+          const bool is_long = live && len == kCtaLong;
+          ct_acc_add(ab_u + e.x * 8u, (double)__uint_as_float(e.y ^ ((m >> 8) << 31)),
+                     live && !is_long && (uint32_t)j < len);
+          if (__any_sync(0xffffffffu, is_long)) {  // a row longer than a slot: straight from A, 16 entries per step
+            if (is_long) {
+              const uint32_t *sl = reinterpret_cast<const uint32_t *>(sb + (size_t)(s0 + r) * 128);
               const int64_t rs = (int64_t)(((uint64_t)sl[1] << 32) | sl[0]);
               const int rl = (int)sl[2];
+              const bool neg = (m >> 8) != 0;
               for (int qq = j; qq < rl; qq += 16) {
                 const float x = __ldg(av + rs + qq);
-                ab[__ldg(aix + rs + qq)] += (double)(neg ? -x : x);
+                const uint32_t a = ab_u + (uint32_t)__ldg(aix + rs + qq) * 8u;
+                ct_stsf64(a, ct_ldsf64(a) + (double)(neg ? -x : x));
               }
             }
           }

@@ -348,18 +348,61 @@ class SparseEmbedding(SketchOperator):
                 self._window = cached = (w.value, pos, wpi)
             return cached
 
-    def _window_eligible(self, indptr, indices, vals, d: int, nnz: int) -> bool:
-        """The row-window kernel is opt-in (``SKT_CSR_WINDOW=1``): bit-identical,
-        but measured slower than csr_tile on config 4 (0.50 vs 0.26 ms, DESIGN.md
-        section 4).  It takes fp32 values, int32 column indices and 16-byte
-        aligned arrays."""
-        if os.environ.get("SKT_CSR_WINDOW", "0") != "1":
-            return False
+    def cta_plan(self, d: int):
+        """Plan of the window gather kernel (csrc/csr_cta.cuh): ``(W, wrows,
+        wpi)`` -- rows per window, the rows of every window stably sorted by
+        bucket (sign in bit 31) and every bucket's first rank per window -- or
+        None when (t, d) is outside the kernel's range.  Cached."""
+        L = _lib.lib()
+        m = self.row_end - self.row_begin
+        w, nwin = ctypes.c_int32(), ctypes.c_int32()
+        with torch.cuda.device(self.device):
+            check(L.skt_csr_cta_config(m, self.output_dim, d, ctypes.byref(w), ctypes.byref(nwin)))
+        if w.value == 0:
+            return None
+        with self._plan_lock:
+            cached = getattr(self, "_cta_plan", None)
+            if cached is None or cached[0] != w.value:
+                pos = torch.empty(m, dtype=torch.int32, device=self.device)
+                wrows = torch.empty(m, dtype=torch.int32, device=self.device)
+                wpi = torch.empty((nwin.value, self.output_dim + 1), dtype=torch.int32, device=self.device)
+                with torch.cuda.device(self.device):
+                    st = _stream_ptr(self.device)
+                    check(L.skt_plan_window_build(_ptr(self.plan_indptr), _ptr(self.plan_rows), self.output_dim,
+                                                  m, w.value, _ptr(pos), _ptr(wpi), st))
+                    check(L.skt_plan_window_rows(_ptr(pos), m, w.value, _ptr(wrows), st))
+                self._cta_plan = cached = (w.value, wrows, wpi)
+                self._cta_plan_ws = pos  # alive until the stream has consumed it
+            return cached
+
+    def _window_mode(self, indptr, indices, vals) -> str:
+        """Which row-window CSR kernel takes this input: ``SKT_CSR_WINDOW`` =
+        ``cta`` (window gather, csr_cta.cuh), ``1`` (slot ring through L2,
+        csr_window.cuh) or unset / ``0`` (the per-bucket kernels).  Both take
+        fp32 values and int32 column indices."""
+        mode = os.environ.get("SKT_CSR_WINDOW", "0")
+        if mode not in ("1", "cta") or self.row_end - self.row_begin <= 0:
+            return ""
         if vals.dtype != torch.float32 or indices.dtype != torch.int32:
-            return False
-        if any(x.data_ptr() % 16 for x in (vals, indices, indptr)):
-            return False
-        return self.row_end - self.row_begin > 0
+            return ""
+        if mode == "1" and any(x.data_ptr() % 16 for x in (vals, indices, indptr)):
+            return ""
+        return mode
+
+    def _window_eligible(self, indptr, indices, vals, d: int, nnz: int) -> bool:
+        return self._window_mode(indptr, indices, vals) != ""
+
+    def _apply_csr_cta(self, plan, indptr, indices, vals, d: int, out):
+        w, wrows, wpi = plan
+        with torch.cuda.device(self.device):
+            check(
+                _lib.lib().skt_apply_csr_cta(
+                    _ptr(wrows), _ptr(wpi), w, self.output_dim, self.row_end - self.row_begin, _ptr(indptr),
+                    _ITYPE[indptr.dtype], _ptr(indices), _ptr(vals), vals.numel(), d, _ptr(out),
+                    _TORCH_TO_SKT[out.dtype], max(out.stride(0), 1), _stream_ptr(self.device),
+                )
+            )
+        return out
 
     def _apply_csr_window(self, plan, indptr, indices, vals, d: int, out):
         L = _lib.lib()
@@ -537,12 +580,16 @@ class SparseEmbedding(SketchOperator):
             # wide SA rows (config 5): the column-sweep kernel, shared-memory
             # fp64 accumulators per 8192-column super-step, no global atomics
             return self._apply_csr_wide(indptr, indices, vals, d, out, b0, b1)
-        if (shift is None and deterministic and canonical and b0 == 0 and b1 == self.output_dim and d > 0
-                and self._window_eligible(indptr, indices, vals, d, vals.numel())):
-            # opt-in: A streamed once in row order (csr_window.cuh)
-            plan = self.window_plan(d)
-            if plan is not None:
-                return self._apply_csr_window(plan, indptr, indices, vals, d, out)
+        if shift is None and deterministic and canonical and b0 == 0 and b1 == self.output_dim and d > 0:
+            mode = self._window_mode(indptr, indices, vals)
+            if mode == "cta":  # opt-in: window gather, buckets owned by SMs (csr_cta.cuh)
+                plan = self.cta_plan(d)
+                if plan is not None:
+                    return self._apply_csr_cta(plan, indptr, indices, vals, d, out)
+            elif mode == "1":  # opt-in: A streamed once in row order (csr_window.cuh)
+                plan = self.window_plan(d)
+                if plan is not None:
+                    return self._apply_csr_window(plan, indptr, indices, vals, d, out)
         if shift is None:
             shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
         if b0 % (1 << shift):

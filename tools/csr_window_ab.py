@@ -20,7 +20,6 @@ def small_cases(torch, SparseEmbedding, dev):
     import numpy as np
     import scipy.sparse as sp
 
-    os.environ["SKT_CSR_WINDOW"] = "1"
     rng = np.random.default_rng(5)
     ok = True
     for (n, d, t, dens, longfrac, i64) in [
@@ -47,7 +46,7 @@ def small_cases(torch, SparseEmbedding, dev):
         for odt in (torch.float64, torch.float32):
             ref = op._apply_csr_device(ip, ix, vv, d, odt, True, shift=0)
             assert op._window_eligible(ip, ix, vv, d, vv.numel())
-            plan = op.window_plan(d)
+            plan = op.cta_plan(d) if os.environ["SKT_CSR_WINDOW"] == "cta" else op.window_plan(d)
             if plan is None:
                 print(f"n={n} d={d} t={t}: window kernel not applicable", flush=True)
                 continue
@@ -66,6 +65,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--small-only", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
+    ap.add_argument("--kernel", default="1", choices=["1", "cta"], help="1: csr_window, cta: csr_cta")
     args = ap.parse_args()
     import torch
 
@@ -73,7 +73,7 @@ def main():
     from paper_1207_6365_b200 import SparseEmbedding
 
     dev = torch.device("cuda:0")
-    os.environ["SKT_CSR_WINDOW"] = "1"  # the kernel is opt-in
+    os.environ["SKT_CSR_WINDOW"] = args.kernel  # the kernels are opt-in
     if not args.skip_small:
         ok = small_cases(torch, SparseEmbedding, dev)
         print("small cases:", "OK" if ok else "MISMATCH", flush=True)
@@ -87,8 +87,7 @@ def main():
     ref = op._apply_csr_device(ip, ix, vv, cfg["d"], odt, True, shift=0)
     got = op._apply_csr_device(ip, ix, vv, cfg["d"], odt, True)
     torch.cuda.synchronize()
-    print("window plan:", None if op.window_plan(cfg["d"]) is None else op.window_plan(cfg["d"])[0],
-          "bit-identical to csr_tile:", bool(torch.equal(got.view(torch.int32), ref.view(torch.int32))), flush=True)
+    print("kernel", args.kernel, "bit-identical to csr_tile:", bool(torch.equal(got.view(torch.int32), ref.view(torch.int32))), flush=True)
     for name, kw in (("csr_tile", dict(shift=0)), ("csr_window", dict())):
         out = torch.empty_like(ref)
         times = []
