@@ -2,7 +2,7 @@
 # other configs, K5 fp32/fp64, torchrun N=1, the reference suite through the
 # shim, and the ncu launch list + full capture of the headline kernel
 cd $GRAFT_REPO_ROOT
-F=gpurun_out/final3; mkdir -p $F
+F=gpurun_out/final4; mkdir -p $F
 nproc > $F/nproc.txt; nvidia-smi -q | head -40 > $F/nvsmi.txt
 timeout 1500 python -m pytest tests/ -q -m gpu > $F/pytest_gpu.log 2>&1; echo rc_pytest=$?
 python -c "import __graft_entry__ as g; g.smoke()" > $F/smoke.log 2>&1; echo rc_smoke=$?
@@ -20,3 +20,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:dens
 ncu -i /tmp/prof_c3.ncu-rep --page raw --csv > $F/prof_c3.raw.csv 2>&1
 ncu -i /tmp/prof_c3.ncu-rep --page details --csv > $F/prof_c3.details.csv 2>&1
 timeout 300 python tools/csr_window_ab.py --skip-small > $F/window_ab.log 2>&1; echo rc_window=$?
+timeout 300 python tools/csr_window_ab.py --skip-small --kernel cta > $F/cta_ab.log 2>&1; echo rc_cta=$?
