@@ -95,7 +95,17 @@ skt_status win_launch(const WinParams &p, int chunks, int G, size_t smem, cudaSt
   auto k = chunks <= 1 ? csr_window_kernel<IP, TOut, 1>
                        : chunks <= 2 ? csr_window_kernel<IP, TOut, 2> : csr_window_kernel<IP, TOut, 4>;
   SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
-  SKT_LAUNCH(k, (unsigned)G, kWinThreads, smem, s, p);
+  // The scatter and accumulate warps of different CTAs wait on each other, so all
+  // G CTAs must be resident at once: a cooperative launch fails (instead of
+  // hanging) when the device cannot hold them.
+  WinParams pc = p;
+  void *args[] = {(void *)&pc};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k, dim3((unsigned)G), dim3(kWinThreads), args, smem, s);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(SKT_ENOTSUP, fn, std::string("the row-window kernel needs all its CTAs resident: ") + cudaGetErrorString(e));
+  }
   return check_launch(fn);
 }
 }  // namespace

@@ -589,7 +589,11 @@ class SparseEmbedding(SketchOperator):
             elif mode == "1":  # opt-in: A streamed once in row order (csr_window.cuh)
                 plan = self.window_plan(d)
                 if plan is not None:
-                    return self._apply_csr_window(plan, indptr, indices, vals, d, out)
+                    try:
+                        return self._apply_csr_window(plan, indptr, indices, vals, d, out)
+                    except _lib.SketchError as e:
+                        if "status 3" not in str(e):  # SKT_ENOTSUP: CTAs not co-resident -> default kernel
+                            raise
         if shift is None:
             shift = self.csr_group_shift(d, canonical, vals.numel()) if deterministic else 0
         if b0 % (1 << shift):
