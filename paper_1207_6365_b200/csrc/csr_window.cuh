@@ -111,9 +111,6 @@ __device__ __forceinline__ void wn_prefetch_l2(const void *src, uint32_t bytes, 
   asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(pol)
                : "memory");
 }
-__device__ __forceinline__ void wn_st_slot(void *p, uint32_t a, uint32_t b, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
-}
 __device__ __forceinline__ void wn_st_slot4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b), "r"(c),
                "r"(d), "l"(pol));
