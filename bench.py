@@ -730,12 +730,20 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # W >= 3 warm-up steps
     cfg = CONFIGS[args.config]
+    # stdout carries exactly ONE JSON line: anything native libraries print to
+    # fd 1 during the run (NCCL prints its version / INFO lines there when
+    # NCCL_DEBUG is set in the environment) goes to stderr instead
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     if args.kernel == "lowrank":
         line = lowrank_report(args, cfg)
     else:
         line = reference_arm(args, cfg) if args.impl == "reference" else our_arm(args, cfg)
+    sys.stdout.flush()
     if line is not None:
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
+    os.close(json_fd)
 
 
 if __name__ == "__main__":
