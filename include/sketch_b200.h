@@ -147,8 +147,9 @@ skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint6
                               int64_t d, void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws,
                               size_t ws_bytes, void *stream);
 
-/* Row-window kernel for canonical CSR (csrc/csr_window.cuh): the same contract
- * and bit-identical result as skt_apply_csr, for fp32 values / int32 column
+/* Row-window kernel for canonical CSR (csrc/csr_window.cuh; replaces
+ * sketch.py:155-164 like skt_apply_csr): the same contract and bit-identical
+ * result as skt_apply_csr, for fp32 values / int32 column
  * indices with rows of about 16 stored entries and an m x d fp64 SA that fits
  * the chip's shared memory (BASELINE config 4).  A is streamed ONCE in row
  * order: rows are cut into windows of W consecutive rows, every row of a
@@ -174,8 +175,9 @@ skt_status skt_apply_csr_window(const uint32_t *pos, const int32_t *wpi, int32_t
                                 void *sa, skt_dtype sa_dtype, int64_t ldsa, void *ws, size_t ws_bytes,
                                 void *stream);
 
-/* Window gather kernel for canonical CSR (csrc/csr_cta.cuh): same contract and
- * bit-identical result as skt_apply_csr, fp32 values / int32 column indices,
+/* Window gather kernel for canonical CSR (csrc/csr_cta.cuh; replaces
+ * sketch.py:155-164 like skt_apply_csr): same contract and bit-identical
+ * result as skt_apply_csr, fp32 values / int32 column indices,
  * m x d fp64 accumulators within the chip's shared memory.  Every SM owns a
  * contiguous bucket range; all SMs walk A window by window (rows of a window
  * stably sorted by bucket: wrows = the inverse of skt_plan_window_build's pos,
