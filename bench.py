@@ -148,7 +148,7 @@ def dominant_kernel(cfg, lev: bool, args, sa_dt) -> str:
     if args.fast:
         return "csr_atomic_kernel (fast mode: unordered RED.ADD)"
     if cfg["d"] > 25_000:
-        return "csr_part_scatter + csr_part_accum (deterministic wide-d: partition by column block, then per-block accumulate)"
+        return "csr_fine_scatter + csr_fine_accum (deterministic wide-d: entries ordered by 1024-column block, then a warp per (bucket, block) adds in row order)"
     return "csr_group_kernel (grouped sweep)" if cfg.get("per_row", 16) <= 8 else "csr_tile_kernel (densify tiles)"
 
 

@@ -1,9 +1,11 @@
-"""The wide-CSR kernels behind skt_apply_csr_wide (csrc/csr_partition.cuh, the
-default; csrc/csr_colblock.cuh, opt-in) for CSR A with SA rows too wide for
-on-chip accumulators (BASELINE config 5's shape): bit-exact against the oracle
-(sketch.py:155-164: per output, ascending row order from +0.0) on the edge
-cases of their design -- several 16384-column blocks and a partial last one,
-buckets of more than 512 rows (several pieces), empty buckets and empty rows,
+"""The wide-CSR kernels behind skt_apply_csr_wide (csrc/csr_fine.cuh, the
+default; csrc/csr_partition.cuh and csrc/csr_colblock.cuh, opt-in) for CSR A
+with SA rows too wide for on-chip accumulators (BASELINE config 5's shape):
+bit-exact against the oracle (sketch.py:155-164: per output, ascending row
+order from +0.0) on the edge cases of their design -- several column blocks and
+a partial last one, buckets of more than 32 / 512 rows (several pieces, more
+than 32 pieces), pieces too large for the shared-memory image, empty buckets
+and empty rows,
 rows with thousands of entries in one block, a column shared by every row of a
 bucket (chains longer than 32 and lists over 2048 entries: the ordered
 fallback), int64 index arrays, fp64 values, fp32 / fp64 output, bucket
@@ -76,6 +78,20 @@ def test_colsweep_dense_runs_and_shared_columns():
     _check(SparseEmbedding(n, t, 9), a, t, 9, d)
 
 
+def test_fine_blocks_over_256_and_unstaged_piece():
+    """More than 256 column blocks (d > 262,144) and an fp32 piece with more
+    entries than the shared-memory image holds (placed directly in the
+    workspace), next to ordinary pieces."""
+    rng = np.random.default_rng(11)
+    n, d, t = 1_200, 300_001, 3
+    a = _random_csr(rng, n, d, 30, np.float32).tolil()
+    for r in (5, 600):
+        a[r, 1000:21_000] = rng.standard_normal(20_000).astype(np.float32)
+    a = sp.csr_array(a)
+    a.sort_indices()
+    _check(SparseEmbedding(n, t, 13), a, t, 13, d)
+
+
 def test_colsweep_int64_indices_and_empty_rows():
     rng = np.random.default_rng(2)
     n, d, t = 4_000, 33_000, 29
@@ -109,10 +125,11 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("kernel", ["colblock"])
+@pytest.mark.parametrize("kernel", ["colblock", "partition"])
 def test_wide_kernel_opt_in(kernel):
-    """The opt-in single-kernel wide path (SKT_CSR_WIDE=colblock:
-    csr_colblock.cuh; the default is the partition path, csr_partition.cuh),
+    """The opt-in wide paths (SKT_CSR_WIDE=colblock: csr_colblock.cuh, one
+    kernel; SKT_CSR_WIDE=partition: csr_partition.cuh, 16384-column blocks; the
+    default is the fine-block path, csr_fine.cuh),
     run in a child process (the selector is read once per process): bit-exact
     against the oracle."""
     import os
