@@ -37,16 +37,29 @@ namespace {
 constexpr int kFbShift = SKT_FB_SHIFT;
 constexpr int kFbCols = 1 << kFbShift;  // 1024 columns per block (2048: 1.05 ms vs 0.94 ms on config 5)
 constexpr int kFbMaxBlocks = 512;
-constexpr int kFpRows = 32;       // rows per piece
-constexpr int kFsThreads = 512;   // F3 threads
-constexpr int kFsUnroll = 4;      // F3: 32-entry batches of a row in flight
+#ifndef SKT_FP_ROWS
+#define SKT_FP_ROWS 32
+#endif
+constexpr int kFpRows = SKT_FP_ROWS;  // rows per piece (<= 32: lane per row)
+#ifndef SKT_FS_THREADS
+#define SKT_FS_THREADS 512
+#endif
+constexpr int kFsThreads = SKT_FS_THREADS;  // F3 threads
+#ifndef SKT_FS_UNROLL_MARK
+#define SKT_FS_UNROLL_MARK 8
+#endif
+#ifndef SKT_FS_UNROLL
+#define SKT_FS_UNROLL 8
+#endif
+constexpr int kFsUnroll = SKT_FS_UNROLL;           // F3: 32-entry batches of a row in flight (entries)
+constexpr int kFsUnrollMark = SKT_FS_UNROLL_MARK;  // ... (run marks)
 constexpr int kFaWarps = SKT_FA_WARPS;  // F4 warps (units) per CTA
 constexpr int kFaUnroll = 4;      // F4: steps with loads in flight
 constexpr int kFaWarpBytes = kFbCols * 8 + kFbCols + 512;  // accumulators, column tags, region tables
 
 // entries of a piece staged in shared memory (F3)
 template <typename TV>
-__host__ __device__ constexpr int fine_cap() { return sizeof(TV) == 4 ? 12288 : 8192; }
+__host__ __device__ constexpr int fine_cap() { return kFpRows * (sizeof(TV) == 4 ? 384 : 256); }
 
 inline int fine_nblk(int64_t d) { return (int)std::max<int64_t>(1, (d + kFbCols - 1) / kFbCols); }
 
@@ -68,7 +81,7 @@ __global__ void __launch_bounds__(256) csr_fine_piece_nnz_kernel(const int64_t *
   const int64_t b = piece_bucket(pstart, t, j);
   const int64_t g = pindptr[b] + (j - pstart[b]) * kFpRows + lane;
   int64_t s = 0;
-  if (g < pindptr[b + 1]) {
+  if (lane < kFpRows && g < pindptr[b + 1]) {
     const int64_t row = __ldg(prow + g) & 0x7fffffffu;
     s = (int64_t)aip[row + 1] - (int64_t)aip[row];
   }
@@ -86,7 +99,7 @@ inline size_t fine_scatter_smem(int nblk, size_t vsize) {
 // F3: CTA per piece.  reg[j * (nblk + 1) + q] = first workspace slot of the
 // piece's block-q region (q = nblk: the end of the piece's entries).
 template <typename IP, typename IX, typename TV>
-__global__ void __launch_bounds__(kFsThreads, 2) csr_fine_scatter_kernel(
+__global__ void __launch_bounds__(kFsThreads, 1024 / kFsThreads) csr_fine_scatter_kernel(
     const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
     const int64_t *__restrict__ pstart, const int64_t *__restrict__ pbase, int nblk, const IP *__restrict__ aip,
     const IX *__restrict__ aix, const TV *__restrict__ av, int64_t *__restrict__ reg, uint16_t *__restrict__ wkey,
@@ -142,12 +155,13 @@ __global__ void __launch_bounds__(kFsThreads, 2) csr_fine_scatter_kernel(
       carry = __shfl_sync(0xffffffffu, q, 31);
     };
     int k0 = 0;
-    for (; k0 + 32 * U <= len; k0 += 32 * U) {
-      int qs[U];
+    for (; k0 + 32 * kFsUnrollMark <= len; k0 += 32 * kFsUnrollMark) {
+      int qs[kFsUnrollMark];
 #pragma unroll
-      for (int u = 0; u < U; ++u) qs[u] = (int)((int64_t)__ldg(ix + k0 + 32 * u) >> kFbShift);  // canonical: < nblk
+      for (int u = 0; u < kFsUnrollMark; ++u)
+        qs[u] = (int)((int64_t)__ldg(ix + k0 + 32 * u) >> kFbShift);  // canonical: < nblk
 #pragma unroll
-      for (int u = 0; u < U; ++u) mark(qs[u], k0 + 32 * u + lane);
+      for (int u = 0; u < kFsUnrollMark; ++u) mark(qs[u], k0 + 32 * u + lane);
     }
     for (; k0 < len; k0 += 32) {
       const int k = k0 + lane;
