@@ -47,6 +47,28 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 
 constexpr int kNumSMs = 148;
 
+// ---- CSR row extents of 32 scattered rows ----------------------------------
+// Lane l holds row id `row` (< 0: none) and gets (start, length) of that row.
+// indptr[row] and indptr[row + 1] share a 128-byte line, so instead of one
+// gather of the 32 starts and one of the 32 ends (32 lines each), the first
+// load reads start and end of the rows of lanes 0..15 (lanes l and l + 16 read
+// the pair of row l) and the second those of lanes 16..31: 16 lines per load.
+#ifdef __CUDACC__
+template <typename IP>
+__device__ __forceinline__ void row_extent_paired(const IP *__restrict__ aip, int64_t row, int lane, int64_t &rs,
+                                                  int &len) {
+  const int64_t other = __shfl_xor_sync(0xffffffffu, row, 16);
+  const int hi = lane >> 4;  // 0: this half reads starts, 1: ends
+  const int64_t r1 = hi ? other : row, r2 = hi ? row : other;
+  const int64_t x1 = r1 >= 0 ? (int64_t)aip[r1 + hi] : 0;
+  const int64_t x2 = r2 >= 0 ? (int64_t)aip[r2 + hi] : 0;
+  const int64_t s1 = __shfl_xor_sync(0xffffffffu, x1, 16), s2 = __shfl_xor_sync(0xffffffffu, x2, 16);
+  rs = hi ? s2 : x1;
+  len = row >= 0 ? (int)((hi ? x2 : s1) - rs) : 0;
+  if (row < 0) rs = 0;
+}
+#endif
+
 // ---- 128-bit PCG64 -------------------------------------------------------
 typedef unsigned __int128 u128;
 

@@ -44,13 +44,9 @@ __global__ void __launch_bounds__(kGroupWarps * 32) csr_group_kernel(
   // packed (bucket-in-group | neg << 8); plan words of the next chunk.
   uint32_t wc = beg + lane < end ? __ldg(grow + beg + lane) : 0u;
   uint32_t bc = beg + lane < end ? (uint32_t)(gblo ? __ldg(gblo + beg + lane) : 0) : 0u;
-  int64_t rs_c = 0;
-  int len_c = 0;
-  if (beg + lane < end) {
-    const int64_t row = wc & 0x7fffffffu;
-    rs_c = (int64_t)aip[row];
-    len_c = (int)((int64_t)aip[row + 1] - rs_c);
-  }
+  int64_t rs_c;
+  int len_c;
+  row_extent_paired(aip, beg + lane < end ? (int64_t)(wc & 0x7fffffffu) : (int64_t)-1, lane, rs_c, len_c);
   uint32_t wn = beg + 32 + lane < end ? __ldg(grow + beg + 32 + lane) : 0u;
   uint32_t bn = beg + 32 + lane < end ? (uint32_t)(gblo ? __ldg(gblo + beg + 32 + lane) : 0) : 0u;
 
@@ -73,13 +69,9 @@ __global__ void __launch_bounds__(kGroupWarps * 32) csr_group_kernel(
     }
     const uint32_t longm = __ballot_sync(0xffffffffu, lane < nrows && len_c > G);
     // ---- prefetch: descriptors of the next chunk, plan words of the one after
-    int64_t rs_n = 0;
-    int len_n = 0;
-    if (k0 + 32 + lane < end) {
-      const int64_t row = wn & 0x7fffffffu;
-      rs_n = (int64_t)aip[row];
-      len_n = (int)((int64_t)aip[row + 1] - rs_n);
-    }
+    int64_t rs_n;
+    int len_n;
+    row_extent_paired(aip, k0 + 32 + lane < end ? (int64_t)(wn & 0x7fffffffu) : (int64_t)-1, lane, rs_n, len_n);
     const int64_t k2 = k0 + 64;
     const uint32_t wn2 = k2 + lane < end ? __ldg(grow + k2 + lane) : 0u;
     const uint32_t bn2 = k2 + lane < end ? (uint32_t)(gblo ? __ldg(gblo + k2 + lane) : 0) : 0u;

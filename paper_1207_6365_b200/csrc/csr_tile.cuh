@@ -85,6 +85,9 @@ __device__ __forceinline__ void unscatter_rows(TV *tile, int dp, int lane, const
 
 __device__ __forceinline__ int tile_g(int lmax) { return lmax <= 4 ? 4 : lmax <= 8 ? 8 : 16; }
 
+#ifndef SKT_TILE_PAIRED
+#define SKT_TILE_PAIRED 1
+#endif
 #ifndef SKT_TILE_ONEBUF
 #define SKT_TILE_ONEBUF 1
 #endif
@@ -116,6 +119,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
     return (lane < R && k0 + lane < end) ? __ldg(prow + k0 + lane) : 0u;
   };
   auto row_desc = [&](int64_t k0, uint32_t wd, int64_t &rs, int &len) {
+#if SKT_TILE_PAIRED
+    row_extent_paired(aip, (lane < R && k0 + lane < end) ? (int64_t)(wd & 0x7fffffffu) : (int64_t)-1, lane, rs, len);
+#else
     rs = 0;
     len = 0;
     if (lane < R && k0 + lane < end) {
@@ -123,6 +129,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, SKT_TILE_MINB) csr_tile_kerne
       rs = (int64_t)aip[row];
       len = (int)((int64_t)aip[row + 1] - rs);
     }
+#endif
   };
   // publish a batch's descriptors (lane r = row r) into a slot; returns G
   auto publish = [&](int slot, int64_t k0, int64_t rs, int len, uint32_t wd) -> int {
