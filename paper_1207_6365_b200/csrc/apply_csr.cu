@@ -19,6 +19,7 @@
 #include "csr_group.cuh"
 #include "csr_lane.cuh"
 #include "csr_sweep.cuh"
+#include "csr_quad.cuh"
 #include "csr_tile.cuh"
 #include "csr_wide.cuh"
 
@@ -140,6 +141,15 @@ inline bool force_lane() {
   return on;
 }
 
+// SKT_CSR_KERNEL=tile keeps the tile kernel where the 128-bit-load kernel (csr_quad.cuh) would run (A/B).
+inline bool force_tile() {
+  static const bool on = [] {
+    const char *e = getenv("SKT_CSR_KERNEL");
+    return e && e[0] == 't';
+  }();
+  return on;
+}
+
 template <typename IP, typename IX, typename TV, typename TOut>
 skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *blo, int shift,
                   uint64_t t, int64_t n, const void *aip, const void *aix, const void *av,
@@ -196,6 +206,20 @@ skt_status launch(const int64_t *pindptr, const uint32_t *prow, const uint8_t *b
     SKT_LAUNCH(k, (unsigned)blocks, kGroupWarps * 32, smem, stream, pindptr, prow, blo, ngroups,
                shift, t, (const IP *)aip, (const IX *)aix, (const TV *)av, (int)d, (TOut *)sa, ldsa);
     return check_launch(fn);
+  }
+  // (2a) densify tiles with 128-bit loads: fp32 values, int32 columns, d <= 64, rows of ~8-20
+  // nonzeros, index / value arrays on 16-byte boundaries
+  if constexpr (std::is_same<TV, float>::value && std::is_same<IX, int32_t>::value) {
+    if (canon && shift == 0 && d <= kQuadD && !short_rows && nnz <= 20 * n && !force_lane() && !force_tile() &&
+        ((reinterpret_cast<uintptr_t>(aix) | reinterpret_cast<uintptr_t>(av)) & 15) == 0) {
+      const size_t smem = (size_t)kQuadTileBytes * kQuadWarps;
+      const int64_t blocks = ((int64_t)t + kQuadWarps - 1) / kQuadWarps;
+      auto k = csr_quad_kernel<IP, TOut>;
+      SKT_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), fn);
+      SKT_LAUNCH(k, (unsigned)blocks, kQuadWarps * 32, smem, stream, pindptr, prow, t, (const IP *)aip,
+                 (const int32_t *)aix, (const float *)av, (int)d, (TOut *)sa, ldsa);
+      return check_launch(fn);
+    }
   }
   // (2) densify-in-shared-memory tiles, warp per bucket (longer rows)
   if (canon && shift == 0 && d <= kTileMaxD && !force_lane()) {

@@ -47,6 +47,27 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 
 constexpr int kNumSMs = 148;
 
+// ---- L2 residency hints ---------------------------------------------------
+// Loads that should stay in L2 while a stream of read-once data passes through
+// it (the CSR row pointers next to the gathered index / value segments).
+#ifdef __CUDACC__
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_l2_keep(const int32_t *a, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_l2_keep(const int64_t *a, uint64_t pol) {
+  int64_t v;
+  asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+#endif
+
 // ---- CSR row extents of 32 scattered rows ----------------------------------
 // Lane l holds row id `row` (< 0: none) and gets (start, length) of that row.
 // indptr[row] and indptr[row + 1] share a 128-byte line, so instead of one
