@@ -133,12 +133,14 @@ skt_status skt_apply_csr(const int64_t *indptr, const uint32_t *rows, const uint
  * accumulators (BASELINE config 5: d = 262,144, t = 400) -- same contract and
  * bit-identical result as skt_apply_csr (ascending row order per output from
  * +0.0), for CANONICAL input (sorted, distinct column indices per row: as_csr
- * output), shift-0 plan (indptr, rows).  One CTA per (bucket, column block)
- * accumulates 16384-column blocks with fp64 accumulators in shared memory
- * after a stable partition of the bucket's entries by block; no global
- * atomics.  Workspace (device, caller-owned): skt_apply_csr_wide_workspace(n,
- * t, d, nnz, val_dtype) bytes -- row block boundaries and the partitioned
- * entries (~nnz x (2 + value size) bytes). */
+ * output), shift-0 plan (indptr, rows).  The entries are ordered by
+ * 1024-column block (stable: row order kept) per 32-row piece of a bucket, then
+ * one warp per (bucket, column block) adds them in row order into fp64
+ * accumulators in shared memory (csrc/csr_fine.cuh); no atomics.  d > 524,288
+ * or SKT_CSR_WIDE=partition|colblock: the 16384-column partition path / the
+ * single-kernel column-block path.  Workspace (device, caller-owned):
+ * skt_apply_csr_wide_workspace(n, t, d, nnz, val_dtype) bytes -- the piece
+ * tables and the ordered entries (~nnz x (2 + value size) bytes). */
 skt_status skt_apply_csr_wide_workspace(int64_t n, uint64_t t, int64_t d, int64_t nnz, skt_dtype val_dtype,
                                         size_t *bytes);
 skt_status skt_apply_csr_wide(const int64_t *indptr, const uint32_t *rows, uint64_t t, int64_t n,

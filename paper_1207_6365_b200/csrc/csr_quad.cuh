@@ -34,7 +34,10 @@ namespace {
 #ifndef SKT_QUAD_MINB
 #define SKT_QUAD_MINB 4
 #endif
-constexpr int kQuadWarps = 4;
+#ifndef SKT_QUAD_WARPS
+#define SKT_QUAD_WARPS 4
+#endif
+constexpr int kQuadWarps = SKT_QUAD_WARPS;
 constexpr int kQuadD = 64;                       // tile width (d <= 64)
 constexpr int kQuadTileBytes = 32 * kQuadD * 4;  // per warp
 

@@ -577,8 +577,8 @@ class SparseEmbedding(SketchOperator):
         if not (0 <= b0 < b1 <= self.output_dim):
             raise ValueError(f"bad bucket range {buckets!r}")
         if deterministic and canonical and d > self._CSR_SMEM_MAX_D:
-            # wide SA rows (config 5): the column-sweep kernel, shared-memory
-            # fp64 accumulators per 8192-column super-step, no global atomics
+            # wide SA rows (config 5): entries ordered by 1024-column block, then a warp per
+            # (bucket, block) adds in row order into shared-memory fp64 accumulators; no atomics
             return self._apply_csr_wide(indptr, indices, vals, d, out, b0, b1)
         if shift is None and deterministic and canonical and b0 == 0 and b1 == self.output_dim and d > 0:
             mode = self._window_mode(indptr, indices, vals)
@@ -614,7 +614,7 @@ class SparseEmbedding(SketchOperator):
 
     def _apply_csr_wide(self, indptr, indices, vals, d: int, out, b0: int, b1: int):
         """skt_apply_csr_wide: rows [b0, b1) of SA for canonical CSR A with
-        wide rows (csrc/csr_colsweep.cuh); writes ``out`` directly in its dtype."""
+        wide rows (csrc/csr_fine.cuh); writes ``out`` directly in its dtype."""
         L = _lib.lib()
         m = self.row_end - self.row_begin
         nb = ctypes.c_size_t()

@@ -8,5 +8,7 @@ for k in scatter accum; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:csr_fine_$k -s 3 -c 1 -o $F/fine_$k -f \
     python bench.py --config c5 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $F/ncu_$k.log 2>&1; echo rc_$k=$?
   ncu -i $F/fine_$k.ncu-rep --page details --csv > $F/fine_$k.details.csv 2>&1
+  ncu -i $F/fine_$k.ncu-rep --page raw --csv > $F/fine_$k.raw.csv 2>&1
+  rm -f $F/fine_$k.ncu-rep
 done
 cat $F/plain.json

@@ -7,4 +7,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -
   python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline "$@" > $F/ncu_$n.log 2>&1; echo rc=$?
 ncu -i $F/$n.ncu-rep --page details --csv > $F/$n.details.csv 2>&1
 ncu -i $F/$n.ncu-rep --page source --csv --print-source sass > $F/$n.sass.csv 2>&1
+ncu -i $F/$n.ncu-rep --page raw --csv > $F/$n.raw.csv 2>&1
 [ $(stat -c %s $F/$n.ncu-rep) -gt 40000000 ] && rm -f $F/$n.ncu-rep

@@ -1,8 +1,8 @@
 # round-2 measurement pass: tests, smoke, headline bench + reference arm, the
 # other configs, K5 fp32/fp64, torchrun N=1, the reference suite through the
 # shim, and the ncu launch list + full capture of the headline kernel
-cd $GRAFT_REPO_ROOT
-F=gpurun_out/final5; mkdir -p $F
+cd $GRAFT_REPO_ROOT; rm -rf gpurun_out/*
+F=gpurun_out/final6; mkdir -p $F
 nproc > $F/nproc.txt; nvidia-smi -q | head -40 > $F/nvsmi.txt
 timeout 1500 python -m pytest tests/ -q -m gpu > $F/pytest_gpu.log 2>&1; echo rc_pytest=$?
 python -c "import __graft_entry__ as g; g.smoke()" > $F/smoke.log 2>&1; echo rc_smoke=$?
@@ -23,3 +23,6 @@ timeout 300 python tools/csr_window_ab.py --skip-small > $F/window_ab.log 2>&1; 
 timeout 300 python tools/csr_window_ab.py --skip-small --kernel cta > $F/cta_ab.log 2>&1; echo rc_cta=$?
 bash tools/gpu_fine_ncu.sh > $F/fine_ncu.log 2>&1; echo rc_fine_ncu=$?
 for m in partition colblock; do SKT_CSR_WIDE=$m timeout 300 python tools/wide_ab.py > $F/wide_ab_$m.log 2>&1; done; timeout 300 python tools/wide_ab.py > $F/wide_ab_fine.log 2>&1; echo rc_wide_ab=$?
+bash tools/gpu_ncu_one.sh c4 csr_quad_kernel c4_quad > $F/ncu_quad.log 2>&1; echo rc_ncu_quad=$?
+rm -f gpurun_out/ncu_one/c4_quad.ncu-rep
+SKT_CSR_KERNEL=tile python bench.py --config c4 --no-e2e --no-cpu-baseline > $F/bench_c4_tile.json 2> $F/bench_c4_tile.err; echo rc_c4_tile=$?
