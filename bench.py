@@ -149,7 +149,11 @@ def dominant_kernel(cfg, lev: bool, args, sa_dt) -> str:
         return "csr_atomic_kernel (fast mode: unordered RED.ADD)"
     if cfg["d"] > 25_000:
         return "csr_fine_scatter + csr_fine_accum (deterministic wide-d: entries ordered by 1024-column block, then a warp per (bucket, block) adds in row order)"
-    return "csr_group_kernel (grouped sweep)" if cfg.get("per_row", 16) <= 8 else "csr_tile_kernel (densify tiles)"
+    if cfg.get("per_row", 16) <= 8:
+        return "csr_group_kernel (grouped sweep)"
+    if cfg["dtype"] == "f32" and cfg["d"] <= 64 and os.environ.get("SKT_CSR_KERNEL") not in ("tile", "lane"):
+        return "csr_quad_kernel (densify tiles, 128-bit loads, row pointers kept in L2)"
+    return "csr_tile_kernel (densify tiles)"
 
 
 def traffic_for(cfg_name: str):
@@ -605,8 +609,9 @@ def our_arm(args, cfg):
         # well below streaming HBM: the kernel's ceiling is that access pattern
         roofline["gather_ceiling"] = {
             "ms": gc, "frac": round(gc / kern_ms, 4),
-            "source": "the same access pattern without arithmetic, L2 flushed (tools/gather_bench.cu, "
-                      "profiles/r01_gather_ceiling.json)"}
+            "source": "the bucket-ordered access pattern with 32-bit loads and without arithmetic, L2 flushed "
+                      "(tools/gather_bench.cu, profiles/r01_gather_ceiling.json); csr_quad's 128-bit loads "
+                      "pass it (frac > 1)"}
 
     # ---- end to end through the public API, host buffers
     e2e, e2e_numpy = None, None

@@ -17,8 +17,9 @@
 //     <= 13 entries at any alignment and rows of 16 on a 16-byte boundary; 8
 //     load instructions per 32 rows instead of 32, all issued before use and
 //     in flight while the previous batch is accumulated;
-//   * entries past the 16 slots (long rows) are fetched by the whole warp when
-//     the batch is scattered.
+//   * rows reaching up to 4 slots past the 16 (rows of 14-16 entries off a
+//     16-byte boundary) take one more 128-bit slot group, longer rows the whole
+//     warp per row from slot 16, both when the batch is scattered.
 // Pipeline: batch b scattered / accumulated / cleared, batch b+1's nonzeros in
 // flight, batch b+2's row extents, batch b+3's plan words.
 #pragma once
@@ -137,8 +138,30 @@ __global__ void __launch_bounds__(kQuadWarps * 32, SKT_QUAD_MINB) csr_quad_kerne
       for (int j = 0; j < 4; ++j)
         if (j >= lo && j < hi) trow[cs[j]] = __uint_as_float(__float_as_uint(vs[j]) ^ sg);
     }
-    // rows reaching past their 16 slots: whole warp per row
-    for (uint32_t longm = __ballot_sync(0xffffffffu, ((m0 >> 8) & 3) + (m0 & 0xff) > 16); longm; longm &= longm - 1) {
+    // rows reaching past their 16 slots: up to 20 (rows of 14-16 entries off a 16-byte
+    // boundary) one more 128-bit slot group, read by the row's first lane; longer rows the
+    // whole warp per row from slot 16
+    const int used = ((m0 >> 8) & 3) + (m0 & 0xff);  // slots of row `lane`
+    if (__builtin_expect(__ballot_sync(0xffffffffu, used > 16 && used <= 20) != 0u, 0)) {  // warp-uniform
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const IP b = __shfl_sync(0xffffffffu, b0, 8 * i + g);
+        const int m = mt[i];
+        const int stop = ((m >> 8) & 3) + (m & 0xff);
+        if (q == 0 && stop > 16 && stop <= 20) {
+          const int4 c = __ldg(reinterpret_cast<const int4 *>(aix + b + 16));
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(av + b + 16));
+          const uint32_t sg = (uint32_t)(m >> 16) << 31;
+          float *trow = tile + (8 * i + g) * kQuadD;
+          const int cs[4] = {c.x, c.y, c.z, c.w};
+          const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (16 + j < stop) trow[cs[j]] = __uint_as_float(__float_as_uint(vs[j]) ^ sg);
+        }
+      }
+    }
+    for (uint32_t longm = __ballot_sync(0xffffffffu, used > 20); longm; longm &= longm - 1) {
       const int r = __ffs(longm) - 1;
       const IP b = __shfl_sync(0xffffffffu, b0, r);
       const int m = __shfl_sync(0xffffffffu, m0, r);

@@ -132,6 +132,31 @@ def test_apply_csr_bucket_lane_kernel(dtype, t, d, rng):
         op._apply_csr_device(*dev, d, torch.float64, canonical=False, shift=2)
 
 
+@pytest.mark.parametrize("itype", [np.int32, np.int64])
+@pytest.mark.parametrize("d", [64, 40])
+def test_apply_csr_quad_alignment(itype, d, rng):
+    """csr_quad (fp32 values, int32 columns, d <= 64; 128-bit loads of the 16
+    aligned slots around a row's start): rows of 0..22 entries at every
+    alignment -- entries past the 16 slots take the extra slot group, past 20
+    the whole-warp tail -- plus dense rows; bit-identical for int32 and int64
+    row pointers."""
+    n, t = 40_000, 777
+    lens = rng.integers(0, min(d, 22) + 1, size=n)
+    lens[::97] = d  # dense rows
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(lens)
+    indices = np.concatenate([np.sort(rng.choice(d, size=k, replace=False)) for k in lens]).astype(np.int32)
+    data = rng.standard_normal(indptr[-1]).astype(np.float32)
+    a = sp.csr_array((data, indices, indptr), shape=(n, d))
+    op = SparseEmbedding(n, t, seed=d)
+    h, s = O.hash_signs(n, t, d)
+    ref = O.np_apply_csr(h, s, t, a)
+    dev = [torch.from_numpy(x).cuda() for x in (indptr.astype(itype), indices, data)]
+    for out_dtype in (torch.float64, torch.float32):
+        got = op._apply_csr_device(*dev, d, out_dtype, canonical=True).cpu().numpy()
+        assert np.array_equal(got, ref.astype(got.dtype)), out_dtype
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("d", [64, 100, 200])
 @pytest.mark.parametrize("tile_rows", ["16", "32"])
