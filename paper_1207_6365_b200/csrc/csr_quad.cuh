@@ -42,6 +42,33 @@ constexpr int kQuadWarps = SKT_QUAD_WARPS;
 constexpr int kQuadD = 64;                       // tile width (d <= 64)
 constexpr int kQuadTileBytes = 32 * kQuadD * 4;  // per warp
 
+// Slots 16..19 of the rows of a batch that reach up to 4 slots past their 16
+// (rows of 14-16 entries off a 16-byte boundary): one more 128-bit load of
+// indices and values by the row's first lane, scattered into the tile.
+template <typename IP>
+__device__ __noinline__ void quad_extra_slots(float *tile, const int32_t *__restrict__ aix,
+                                              const float *__restrict__ av, IP b0, int mt0, int mt1, int mt2, int mt3,
+                                              int g, int q) {
+  const int mt[4] = {mt0, mt1, mt2, mt3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const IP b = __shfl_sync(0xffffffffu, b0, 8 * i + g);
+    const int m = mt[i];
+    const int stop = ((m >> 8) & 3) + (m & 0xff);
+    if (q == 0 && stop > 16 && stop <= 20) {
+      const int4 c = __ldg(reinterpret_cast<const int4 *>(aix + b + 16));
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(av + b + 16));
+      const uint32_t sg = (uint32_t)(m >> 16) << 31;
+      float *trow = tile + (8 * i + g) * 64;
+      const int cs[4] = {c.x, c.y, c.z, c.w};
+      const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (16 + j < stop) trow[cs[j]] = __uint_as_float(__float_as_uint(vs[j]) ^ sg);
+    }
+  }
+}
+
 template <typename IP, typename TOut>
 __global__ void __launch_bounds__(kQuadWarps * 32, SKT_QUAD_MINB) csr_quad_kernel(
     const int64_t *__restrict__ pindptr, const uint32_t *__restrict__ prow, uint64_t t,
@@ -142,25 +169,8 @@ __global__ void __launch_bounds__(kQuadWarps * 32, SKT_QUAD_MINB) csr_quad_kerne
     // boundary) one more 128-bit slot group, read by the row's first lane; longer rows the
     // whole warp per row from slot 16
     const int used = ((m0 >> 8) & 3) + (m0 & 0xff);  // slots of row `lane`
-    if (__builtin_expect(__ballot_sync(0xffffffffu, used > 16 && used <= 20) != 0u, 0)) {  // warp-uniform
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const IP b = __shfl_sync(0xffffffffu, b0, 8 * i + g);
-        const int m = mt[i];
-        const int stop = ((m >> 8) & 3) + (m & 0xff);
-        if (q == 0 && stop > 16 && stop <= 20) {
-          const int4 c = __ldg(reinterpret_cast<const int4 *>(aix + b + 16));
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(av + b + 16));
-          const uint32_t sg = (uint32_t)(m >> 16) << 31;
-          float *trow = tile + (8 * i + g) * kQuadD;
-          const int cs[4] = {c.x, c.y, c.z, c.w};
-          const float vs[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (16 + j < stop) trow[cs[j]] = __uint_as_float(__float_as_uint(vs[j]) ^ sg);
-        }
-      }
-    }
+    if (__ballot_sync(0xffffffffu, used > 16 && used <= 20))  // warp-uniform; out of line: rare on aligned data
+      quad_extra_slots<IP>(tile, aix, av, b0, mt[0], mt[1], mt[2], mt[3], g, q);
     for (uint32_t longm = __ballot_sync(0xffffffffu, used > 20); longm; longm &= longm - 1) {
       const int r = __ffs(longm) - 1;
       const IP b = __shfl_sync(0xffffffffu, b0, r);
