@@ -54,7 +54,10 @@ constexpr int kFsThreads = SKT_FS_THREADS;  // F3 threads
 constexpr int kFsUnroll = SKT_FS_UNROLL;           // F3: 32-entry batches of a row in flight (entries)
 constexpr int kFsUnrollMark = SKT_FS_UNROLL_MARK;  // ... (run marks)
 constexpr int kFaWarps = SKT_FA_WARPS;  // F4 warps (units) per CTA
-constexpr int kFaUnroll = 4;      // F4: steps with loads in flight
+#ifndef SKT_FA_UNROLL
+#define SKT_FA_UNROLL 4
+#endif
+constexpr int kFaUnroll = SKT_FA_UNROLL;  // F4: steps with loads in flight (x2: double-buffered)
 constexpr int kFaWarpBytes = kFbCols * 8 + kFbCols + 512;  // accumulators, column tags, region tables
 
 // entries of a piece staged in shared memory (F3)
